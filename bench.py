@@ -1,0 +1,384 @@
+"""Checkpoint-load benchmark (BASELINE.json metric: "checkpoint load GB/s &
+time-to-loaded-model at 1/2/4/8 B200 vs PCIe peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config opt-6.7b] [--mode zerocopy|ce|scatter_ce|scatter_zc]
+                    [--chunk-mib 16] [--streams 2] [--ctas 0] [--no-cpu-baseline]
+
+A "step" is one pass of the whole hot path over the synthetic
+checkpoint already sitting in pinned host DRAM: open the index from its bytes (a1), plan
+chunks (a3), move every partition byte host->HBM (a4), materialise the tensors (a5),
+verify every 1 MiB block's Fletcher-64 on the GPU (a6), complete (a8).  Destinations
+are preallocated (a2; T_alloc is reported separately, Q19).  N=1 runs
+BASELINE configs[1] (OPT-6.7B-shaped, 13.3 GB fp16, 1 partition).  Under torchrun every
+rank loads its own copy of that partition from its own pinned buffer over its own PCIe
+link (weak scaling, no collective: SURVEY §8(e)).
+
+value = payload bytes loaded by all ranks / max-over-ranks device time (GB/s, 10^9).
+The partition (13.3 GB) is ~100x the 126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "checkpoint load GB/s & time-to-loaded-model at 1/2/4/8 B200 vs PCIe peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="opt-6.7b")
+    ap.add_argument("--mode", default="zerocopy", choices=["ce", "zerocopy", "scatter_ce", "scatter_zc"])
+    ap.add_argument("--chunk-mib", type=int, default=16)
+    ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--cpu-sample-gib", type=float, default=4.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-standalone", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, n in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def run_reference(args, rank, world):
+    """Reference arm = the CPU oracle as it stands (oracle/loader.py) on this box's host
+    cores, each step a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import index as oindex, layout as olayout, loader as oloader
+    from synth import models, payload
+
+    inv, seed = models.model_inventory(args.config)
+    budget = int(args.cpu_sample_gib * (1 << 30))
+    # oracle converter over the sample's tensors (prefix of partition 0 in source order)
+    lay = olayout.plan([(t.name, t.device, t.dtype, t.shape, t.nbytes) for t in inv], 4096, 1 << 20)
+    d0 = lay.devices()[0]
+    keep = [i for i, e in enumerate(lay.entries) if e.device == d0 and e.offset + e.size <= budget]
+    sub = [inv[i] for i in keep]
+    tensors = [(t.name, t.device, t.dtype, t.shape, payload.payload_bytes(seed, keep[k], t.nbytes))
+               for k, t in enumerate(sub)]
+    slay, sparts = olayout.convert(tensors, 4096, 1 << 20, args.config)
+    blob = oindex.write(slay)
+    times, got = [], 0
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        got = oloader.load_sample(blob, sparts, budget)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    T = sum(times)
+    v = got * args.steps / T / 1e9
+    line = {"metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": T / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config} (oracle sample: first {got} payload bytes of partition 0)",
+                       "cache": "host-only"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"parse index + copy + verify {got} B of {args.config} partition 0"},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, bufs, idx, inv, seed):
+    """The oracle as it stands, single process (1 core), on a bounded sample of the same
+    pinned partition: parse index, copy tensors, recompute and compare checksums."""
+    from oracle import loader as oloader
+    budget = int(args.cpu_sample_gib * (1 << 30))
+    blob = idx.serialize()
+    src = {idx.partitions[p].device: bufs[p].numpy() for p in bufs}
+    t0 = time.perf_counter()
+    got = oloader.load_sample(blob, src, budget)
+    dt = time.perf_counter() - t0
+    return {"value": got / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{got} payload bytes ({args.cpu_sample_gib} GiB budget) of partition 0: parse index, "
+                      f"copy every tensor, recompute+compare 1 MiB Fletcher-64 blocks; {dt:.1f} s"}
+
+
+def h2d_peak(bufs, bases, torch, gib=4, reps=5):
+    """B_h2d(1): cudaMemcpyAsync from the same pinned buffer into the same destination,
+    >= 4 GiB, best of `reps`."""
+    p = sorted(bufs)[0]
+    n = min(gib << 30, bufs[p].nbytes)
+    src = bufs[p].torch()[:n]
+    dst = bases[p][:n]
+    best = 0.0
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        dst.copy_(src, non_blocking=True)
+        e.record()
+        e.synchronize()
+        best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)
+    return best
+
+
+def standalone_hbm(idx, torch, sllm, reps=5):
+    """K4 (checksum) and K3 (scatter + checksum) on a >= 1 GiB device-resident partition
+    image, timed with CUDA events on the launching stream (HBM roofline)."""
+    p = 0
+    L = idx.partitions[p].length
+    n = min(L, 4 << 30) // (1 << 20) * (1 << 20)
+    src = torch.empty(L, dtype=torch.uint8, device="cuda")
+    src.random_(0, 256)
+    out = torch.empty(-(-n // (1 << 20)), dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    res = {}
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        sllm.block_checksums_device(src.data_ptr(), n, 1 << 20, out.data_ptr(), 0, st)
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    t = min(ts) * 1e-3
+    res["k4"] = {"bytes": n, "ms": t * 1e3, "GBps": n / t / 1e9}
+    # K3: scatter the whole partition image into per-tensor buffers (read L + write payload)
+    _, per = sllm.allocate(idx, {0: 0}, scatter=True)
+    ts = []
+    ok = True
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        try:
+            sllm.materialise_device(idx, p, src.data_ptr(), per, 0, st)
+        except sllm.SllmError as ex:  # random image: checksums cannot match, bytes still move
+            ok = ex.status == 9
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    t = min(ts) * 1e-3
+    payload = idx.info()["payload_bytes"]
+    res["k3"] = {"bytes": L + payload, "ms": t * 1e3, "GBps": (L + payload) / t / 1e9, "status_ok": ok}
+    del per, src, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import torch
+    import paper_2401_14351_b200 as sllm
+    from paper_2401_14351_b200 import workloads
+    from synth import models, payload
+
+    payload.build_csynth()
+    torch.cuda.set_device(local)
+    gpu = local
+    dev = torch.device("cuda", gpu)
+
+    # ---- setup (untimed): synthetic checkpoint packed into pinned DRAM by the converter
+    t0 = time.perf_counter()
+    inv, seed = models.model_inventory(args.config)
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=[0] if world == 1 or
+                                       len(set(t.device for t in inv)) == 1 else [rank], gpu_of={0: gpu, rank: gpu})
+    t_setup = time.perf_counter() - t0
+    blob = idx.serialize()
+    parts = sorted(bufs)
+    gpus = {p: gpu for p in parts}
+    cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, n_streams=args.streams, mode=args.mode,
+                          ctas=args.ctas, profile=True)
+    # a2: destination allocation (reported separately, Q19)
+    torch.cuda.synchronize()
+    ta = time.perf_counter()
+    bases, per_tensor = sllm.allocate(idx, gpus, cfg.scatter, partitions=parts)
+    torch.cuda.synchronize()
+    t_alloc = time.perf_counter() - ta
+    payload_bytes = sum(t.nbytes for t in idx.tensors if t.partition in bufs)
+    raw_bytes = sum(idx.partitions[p].length for p in parts)
+
+    b_h2d = h2d_peak(bufs, bases if not cfg.scatter else {p: torch.empty(min(4 << 30, idx.partitions[p].length),
+                                                                          dtype=torch.uint8, device=dev) for p in parts},
+                     torch)
+    stream = torch.cuda.current_stream(gpu)
+
+    def step(prof: bool):
+        c = sllm.LoadConfig(**{**cfg.__dict__, "profile": prof})
+        ix = sllm.Index.from_bytes(blob)                  # a1: open + validate the index
+        res = sllm.load_start(ix, bufs, gpus, c, bases, per_tensor, {p: stream for p in parts})
+        return res, ix
+
+    for _ in range(args.warmup):
+        res, ix = step(False)
+        res.wait()
+        del res, ix
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = []
+    reports = []
+    with ClockSampler(gpu) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for _ in range(args.steps):
+            res, ix = step(True)
+            reports.append(res.wait())
+            del res, ix
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = payload_bytes * world / (ms_step * 1e-3) / 1e9
+
+    # ---- end-to-end through the public API (a2 allocation + index open + load + wait +
+    #      D2H of the verification word), host wall clock, pinned sources
+    e2e_t = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ix = sllm.Index.from_bytes(blob)
+        res = sllm.load(ix, bufs, gpus, sllm.LoadConfig(**{**cfg.__dict__, "profile": False}))
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+        del res, ix
+    e2e = {"value": payload_bytes * world / min(e2e_t) / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": raw_bytes + sum(idx.partitions[p].n_blocks * 8 for p in parts),
+           "d2h_bytes_per_step": 8 * len(parts), "includes": "torch allocation + index open + load + verify + wait",
+           "time_to_loaded_model_s": min(e2e_t)}
+
+    # ---- roofline of the dominant kernel, from the library's per-launch CUDA events
+    rep = reports[-1]
+    kern_ms = sum(r["t_kernel_ms_sum"] for r in reports) / len(reports)
+    kern_launches = rep["kernel_launches"]
+    kern_bytes = rep["kernel_bytes"]
+    roof = None
+    if args.mode in ("zerocopy", "scatter_zc") and kern_launches:
+        # zero-copy kernel: every byte it reads crosses PCIe -> bound by the host link.
+        # Launches on the S streams overlap, so the kernel's rate is its bytes per step
+        # over the step's device time (the kernel is the only work in the step).
+        achieved = kern_bytes / (ms_step * 1e-3) / 1e9
+        roof = {"bound": "pcie", "achieved": achieved, "peak": b_h2d, "unit": "GB/s", "frac": achieved / b_h2d,
+                "traffic": None, "kernel": "materialise_kernel<store,check,host_src>",
+                "launches_per_step": kern_launches, "avg_launch_ms": kern_ms / max(kern_launches, 1),
+                "peak_source": "cudaMemcpyAsync H2D from the same pinned buffer, 4 GiB, best of 5, this run"}
+    standalone = None
+    if not args.no_standalone and rank == 0:
+        del bases, per_tensor
+        torch.cuda.empty_cache()
+        standalone = standalone_hbm(idx, torch, sllm)
+        hbm = peaks().get("hbm_gbs", 6551.4)
+        k4 = standalone["k4"]
+        standalone["k4"]["frac_hbm"] = k4["GBps"] / hbm
+        standalone["k3"]["frac_hbm"] = standalone["k3"]["GBps"] / hbm
+        if roof is None:
+            roof = {"bound": "hbm", "achieved": k4["GBps"], "peak": hbm, "unit": "GB/s", "frac": k4["GBps"] / hbm,
+                    "traffic": None, "kernel": "materialise_kernel<checksum only> (K4, standalone 4 GiB)"}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, bufs, idx, inv, seed)
+    clocks = clk.summary()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {"workload": args.config, "mode": args.mode, "chunk_mib": args.chunk_mib,
+                           "streams": args.streams, "ctas": args.ctas, "payload_bytes_per_gpu": payload_bytes,
+                           "raw_bytes_per_gpu": raw_bytes, "verify": "fletcher64 per 1 MiB block, every block",
+                           "l2": "inputs 13 GB >> 126 MB L2, no flush needed", "parallelism": f"sharded x{world}"},
+                "time_to_loaded_model_s": ms_step * 1e-3, "t_alloc_s": t_alloc, "t_setup_s": t_setup,
+                "b_h2d_measured_GBps": b_h2d, "frac_h2d": (payload_bytes / (ms_step * 1e-3) / 1e9) / b_h2d,
+                "gpu_launches": int(rep["kernel_launches"]) * args.steps,
+                "copy_calls_per_step": int(rep["copy_calls"]),
+                "clocks": clocks, "e2e": e2e, "roofline": roof, "standalone_hbm": standalone,
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

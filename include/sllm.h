@@ -1,0 +1,299 @@
+/* sllm.h -- C ABI of the B200-native loading-optimized checkpoint loader.
+ *
+ * The operations follow the paper's statement of the loading problem
+ * (ServerlessLLM, arXiv 2401.14351; PAPER.md = /root/reference/PAPER.md):
+ *   - convert a checkpoint into one aligned, metadata-free partition per GPU plus a
+ *     tensor index "that maps tensor names to a tuple of GPU id, offset, and size"
+ *     (§Loading-Optimized Checkpoints);
+ *   - open the index;
+ *   - the model manager "allocates memory on GPUs and loads the binary data" through
+ *     chunk-based, pipelined transfers from pinned memory;
+ *   - tensor address = base + offset;
+ *   - a synchronization "returns when all data is loaded into GPUs".
+ * Integrity checking (per-block Fletcher-64) is the build's addition (Q8).
+ *
+ * Conventions (apply to every function):
+ *   - every call returns sllm_status; SLLM_OK == 0.  Outputs go through out-params,
+ *     which are left untouched on failure.  No exception or abort crosses the ABI;
+ *     sllm_last_error() returns a thread-local message for the last failure on the
+ *     calling thread (valid until that thread's next failing call).
+ *   - "host pointer" = CPU virtual address; "device pointer" = CUDA device address.
+ *   - integers are byte counts unless stated; all on-disk data is little-endian.
+ *   - ownership: the CALLER owns source buffers (pinned host memory) and every
+ *     destination (device memory, typically allocated through PyTorch).  The LIBRARY
+ *     owns sllm_index / sllm_load / sllm_comm objects and their internal scratch
+ *     (staging rings, device checksum tables, streams, worker threads), released by
+ *     the matching *_close / *_free call.
+ *   - thread safety: an sllm_index is immutable after open/seal and may be shared by
+ *     threads; one sllm_load object must not be used from two threads at once.
+ */
+#ifndef SLLM_H_
+#define SLLM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SLLM_API __attribute__((visibility("default")))
+#else
+#define SLLM_API
+#endif
+
+#define SLLM_ABI_VERSION 1
+#define SLLM_MAX_NDIM 8
+
+typedef enum {
+  SLLM_OK = 0,
+  SLLM_E_INVALID = 1,     /* bad argument: null pointer, bad alignment/block/chunk, bad mode   */
+  SLLM_E_CONVERSION = 2,  /* duplicate/empty name, payload != prod(shape)*width, bad dtype */
+  SLLM_E_FORMAT = 3,      /* bad magic/version/flags, truncated, overlap, misaligned   */
+  SLLM_E_LOOKUP = 4,      /* unknown tensor name / index out of range                     */
+  SLLM_E_CAPACITY = 5,    /* destination or buffer too small                                    */
+  SLLM_E_IO = 6,          /* file open/read/write failure                                       */
+  SLLM_E_CUDA = 7,        /* a CUDA runtime call failed (message names it)                      */
+  SLLM_E_NCCL = 8,        /* an NCCL call failed or libnccl could not be loaded                 */
+  SLLM_E_CHECKSUM = 9,    /* a loaded block's Fletcher-64 differs from the index               */
+  SLLM_E_BUSY = 10,       /* the destination set is already being loaded                 */
+  SLLM_E_NOMEM = 11       /* host allocation / pinning failed                                   */
+} sllm_status;
+
+/* dtype codes; widths F16/BF16 2, F32 4, I8/U8 1, I64 8. */
+typedef enum { SLLM_F16 = 0, SLLM_BF16 = 1, SLLM_F32 = 2, SLLM_I8 = 3, SLLM_U8 = 4, SLLM_I64 = 5 } sllm_dtype;
+
+typedef struct sllm_index sllm_index; /* parsed / planned index (opaque)                  */
+typedef struct sllm_load sllm_load;   /* one in-flight load (opaque)                       */
+typedef struct sllm_comm sllm_comm;   /* NCCL communicator for the replicated fan-out      */
+
+SLLM_API const char* sllm_last_error(void);
+SLLM_API int32_t sllm_abi_version(void);
+
+/* ------------------------------------------------------------------------------------
+ * Converter (host only).  SPEC S:43 convert(src, align); layout per PAPER.md P:545-547:
+ * for each device ascending, tensors in source order, offset = align_up(cursor, align),
+ * partition length L_d = align_up(last end, align), padding bytes 0x00 (Q1-Q5).
+ * ------------------------------------------------------------------------------------ */
+typedef struct {
+  const char* name;      /* NUL-terminated UTF-8, unique, non-empty                         */
+  int32_t device_id;     /* logical partition id (>= 0); "target GPU" of P:462              */
+  int32_t dtype;         /* sllm_dtype                                                      */
+  int32_t ndim;          /* 0..8; 0 = scalar                                                */
+  const int64_t* shape;  /* ndim positive dims (may be NULL when ndim == 0)                 */
+  const void* data;      /* host pointer to nbytes of payload; may be NULL for sllm_plan    */
+  uint64_t nbytes;       /* must equal prod(shape) * width(dtype)                           */
+} sllm_src_tensor;
+
+/* Plan the layout of n tensors (no bytes move).  align: power of two >= 16.  block:
+ * checksum block size, power of two multiple of align, or 0 for "no checksums".  The
+ * returned index has zeroed checksum tables until sllm_index_seal / sllm_convert_into.
+ * Errors: SLLM_E_INVALID (align/block), SLLM_E_CONVERSION (names, sizes, dtype, dims). */
+SLLM_API sllm_status sllm_plan(const sllm_src_tensor* tensors, size_t n, uint64_t align, uint64_t block,
+                      const char* model_id, sllm_index** out);
+
+/* Fill caller-provided partition buffers (host pointers, part_bufs[p] of length >= L_p for
+ * partition p in ascending device order) from tensors[i].data -- the same tensors, same
+ * order as given to sllm_plan -- zero all padding, then seal (compute block checksums).
+ * Multi-threaded.  Errors: SLLM_E_INVALID (null data / buffer), SLLM_E_CONVERSION. */
+SLLM_API sllm_status sllm_convert_into(const sllm_src_tensor* tensors, size_t n, sllm_index* plan,
+                              void* const* part_bufs);
+
+/* Compute every block checksum of a planned index from partition buffers the caller has
+ * already filled (plan -> fill -> seal).  part_bufs[p]: host pointer, >= L_p bytes, or
+ * NULL to leave partition p's table untouched (a process that holds only its own
+ * partition).  Multi-threaded. */
+SLLM_API sllm_status sllm_index_seal(sllm_index* index, const void* const* part_bufs);
+
+/* convert() to files: <out_dir>/part_<device>.bin and <out_dir>/index.bin. */
+SLLM_API sllm_status sllm_convert(const sllm_src_tensor* tensors, size_t n, uint64_t align, uint64_t block,
+                         const char* model_id, const char* out_dir);
+
+/* Serialize the index (binary format of DESIGN.md §Index format).  If buf is NULL or cap
+ * is too small, *len receives the required size and SLLM_E_CAPACITY is returned (unless
+ * buf is NULL, which returns SLLM_OK with *len set). */
+SLLM_API sllm_status sllm_index_serialize(const sllm_index* index, void* buf, size_t cap, size_t* len);
+
+/* ------------------------------------------------------------------------------------
+ * Index (S:52 read_index, S:61 tensor_address).
+ * ------------------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t align, block, payload_bytes;
+  uint64_t n_partitions, n_tensors;
+  const char* model_id;  /* owned by the index */
+} sllm_index_info;
+
+typedef struct {
+  const char* name;      /* owned by the index */
+  int32_t device_id;
+  int32_t partition;     /* position of the tensor's partition in ascending device order */
+  int32_t dtype;
+  int32_t ndim;
+  int64_t shape[SLLM_MAX_NDIM];
+  uint64_t offset;       /* byte offset inside the partition (multiple of align) */
+  uint64_t nbytes;
+} sllm_tensor_info;
+
+/* Parse + fully validate (every check of DESIGN.md §Index format -> SLLM_E_FORMAT). */
+SLLM_API sllm_status sllm_index_open(const char* path, sllm_index** out);
+SLLM_API sllm_status sllm_index_from_memory(const void* blob, size_t len, sllm_index** out);
+SLLM_API void sllm_index_close(sllm_index* index);
+SLLM_API sllm_status sllm_index_get_info(const sllm_index* index, sllm_index_info* out);
+/* Partition p (0..n_partitions-1, ascending device id). */
+SLLM_API sllm_status sllm_index_partition(const sllm_index* index, size_t p, int32_t* device_id,
+                                 uint64_t* length, uint64_t* n_blocks, uint64_t* n_tensors);
+/* Pointer to partition p's n_blocks block checksums (owned by the index). */
+SLLM_API sllm_status sllm_index_block_checksums(const sllm_index* index, size_t p, const uint64_t** table);
+/* Tensor i in global source order. */
+SLLM_API sllm_status sllm_index_tensor(const sllm_index* index, size_t i, sllm_tensor_info* out);
+SLLM_API sllm_status sllm_index_find(const sllm_index* index, const char* name, size_t* i); /* SLLM_E_LOOKUP */
+/* P:549 base + offset: base_by_partition[p] is partition p's base address (any address
+ * space; the library never dereferences it). */
+SLLM_API sllm_status sllm_tensor_address(const sllm_index* index, const char* name, const uint64_t* base_by_partition,
+                                int32_t* device_id, uint64_t* addr);
+
+/* Fletcher-64 (Q8) of a host buffer; nbytes need not be a multiple of 4
+ * (tail zero-padded).  Host-only helper used by the converter. */
+SLLM_API sllm_status sllm_fletcher64_host(const void* data, uint64_t nbytes, uint64_t* out);
+
+/* Chunk plan (equal chunks except the last): number of chunks of `chunk` bytes
+ * covering `length` bytes. */
+SLLM_API sllm_status sllm_chunk_count(uint64_t length, uint64_t chunk, uint64_t* n_chunks);
+/* Replicated fan-out slices: cut [0, length) into nranks contiguous,
+ * chunk-aligned slices; lo_hi receives 2*nranks values {lo_0, hi_0, lo_1, hi_1, ...}.
+ * Slices are balanced in whole chunks; trailing slices may be empty. */
+SLLM_API sllm_status sllm_replica_slices(uint64_t length, uint64_t chunk, int32_t nranks, uint64_t* lo_hi);
+
+/* ------------------------------------------------------------------------------------
+ * Pinned host memory (the DRAM tier).  Page-locked, mapped into the
+ * device address space (zero-copy capable) and portable across devices.  gpu >= 0
+ * places the pages on that GPU's NUMA node when the system has several nodes.
+ * ------------------------------------------------------------------------------------ */
+SLLM_API sllm_status sllm_host_alloc(uint64_t bytes, int32_t gpu, void** p);
+SLLM_API void sllm_host_free(void* p);
+/* Page-lock + map caller-owned memory (e.g. a NumPy array) so it can be a load source. */
+SLLM_API sllm_status sllm_host_register(void* p, uint64_t bytes);
+SLLM_API sllm_status sllm_host_unregister(void* p);
+/* File -> pinned DRAM tier: read <dir>/part_<device>.bin of partition p into dst (host
+ * pointer, >= L_p bytes), O_DIRECT when possible, `threads` readers (0 = default). */
+SLLM_API sllm_status sllm_host_read_partition(const char* dir, const sllm_index* index, size_t p, void* dst,
+                                     int32_t threads);
+
+/* ------------------------------------------------------------------------------------
+ * Load (S:115 load()).
+ * ------------------------------------------------------------------------------------ */
+typedef enum {
+  SLLM_MODE_CE = 0,         /* copy engine per chunk into base+off, then checksum kernel     */
+  SLLM_MODE_ZEROCOPY = 1,   /* SM-issued 16 B reads of host-mapped memory -> base+off, fused checksum */
+  SLLM_MODE_SCATTER_CE = 2, /* copy engine into a staging ring, then index-driven scatter kernel */
+  SLLM_MODE_SCATTER_ZC = 3  /* SM-issued host reads scattered straight into per-tensor buffers */
+} sllm_mode;
+
+typedef enum { SLLM_FANOUT_NONE = 0, SLLM_FANOUT_BCAST = 1 } sllm_fanout;
+
+typedef struct {
+  uint64_t chunk_bytes; /* multiple of the index block size (and of align); 0 = 16 MiB    */
+  int32_t n_streams;    /* internal streams per GPU, 1..8 (0 = 2)                           */
+  int32_t mode;         /* sllm_mode                                                        */
+  int32_t fanout;       /* sllm_fanout; BCAST requires a comm and a 1-partition index       */
+  int32_t verify;       /* 1 = check every block's Fletcher-64 against the index            */
+  int32_t ctas;         /* CTAs per kernel launch (0 = mode default)                        */
+  int32_t profile;      /* 1 = time every launch/copy with CUDA events (report t_*_ms_sum)  */
+} sllm_load_config;
+
+typedef struct {
+  uint64_t payload_bytes;      /* sum of tensor sizes in the partitions this call loaded    */
+  uint64_t transferred_bytes;  /* host->device bytes moved by this process (PCIe)           */
+  uint64_t fanout_bytes;       /* bytes received through the NVLink fan-out                 */
+  uint64_t chunks;             /* chunks issued                                             */
+  uint64_t kernel_launches;    /* library kernels launched                                  */
+  uint64_t copy_calls;         /* cudaMemcpyAsync calls issued                              */
+  uint64_t t_total_ns;         /* host clock, sllm_load_start entry -> sllm_load_wait exit  */
+  uint64_t t_issue_ns_max;     /* longest per-partition host issue time                     */
+  double t_device_ms_max;      /* longest per-partition device time (CUDA events)           */
+  double t_kernel_ms_sum;      /* profile: summed device time of the load's kernel launches */
+  double t_copy_ms_sum;        /* profile: summed device time of its cudaMemcpyAsync calls */
+  uint64_t kernel_bytes;       /* profile: partition bytes covered by those kernel launches */
+  int32_t bad_partition;       /* -1 when OK                                                */
+  int32_t mode;
+  uint64_t bad_block;          /* UINT64_MAX when OK                                        */
+} sllm_load_report;
+
+/* Communicator for SLLM_FANOUT_BCAST.  One process per GPU: rank 0 calls
+ * sllm_comm_unique_id, the caller distributes the 128 bytes (e.g. via torch.distributed),
+ * every rank calls sllm_comm_init_rank.  Single process, several GPUs: sllm_comm_init_all
+ * (one comm per listed GPU; handle i belongs to gpus[i]).  libnccl.so.2 is loaded lazily. */
+SLLM_API sllm_status sllm_comm_unique_id(void* id128);
+SLLM_API sllm_status sllm_comm_init_rank(const void* id128, int32_t nranks, int32_t rank, int32_t gpu, sllm_comm** out);
+SLLM_API sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_comm** out /* n handles */);
+SLLM_API void sllm_comm_free(sllm_comm* comm);
+
+/* Start loading (asynchronous: returns once worker threads are launched).
+ *   index          : opened/sealed index (must outlive the load).
+ *   cfg            : NULL = defaults (16 MiB chunks, 2 streams, CE, verify).
+ *   host_src[p]    : host pointer to partition p's bytes (pinned via sllm_host_alloc /
+ *                    sllm_host_register or cudaHostAlloc), or NULL = partition not
+ *                    loaded by this call.  For FANOUT_BCAST only the rank's slice is read.
+ *   gpu[p]         : CUDA device ordinal for partition p (ignored if host_src[p] NULL).
+ *   dst_base[p]    : device pointer, >= L_p bytes (contiguous modes and FANOUT); the
+ *                    tensors are views base+offset.  May be NULL in scatter modes.
+ *   dst_tensor[i]  : scatter modes only: device pointer to tensor i's own buffer (>= its
+ *                    nbytes, 16-byte aligned), global source order; NULL entries for
+ *                    tensors of unloaded partitions.  NULL array for contiguous modes.
+ *   stream[p]      : optional caller cudaStream_t (as void*) for partition p.  The load is
+ *                    ordered after work already queued on it, and the stream is made to
+ *                    wait for the load's completion, so work queued on it after
+ *                    sllm_load_start sees the loaded bytes.  NULL array/entry = no ordering.
+ *   comm           : NULL unless cfg->fanout == SLLM_FANOUT_BCAST.
+ * Returns SLLM_E_BUSY if one of dst_base/dst_tensor is the target of an unfinished load.
+ * Tensor contents are defined only after sllm_load_wait returns SLLM_OK (Q17). */
+SLLM_API sllm_status sllm_load_start(const sllm_index* index, const sllm_load_config* cfg,
+                            const void* const* host_src, const int32_t* gpu,
+                            void* const* dst_base, void* const* dst_tensor,
+                            void* const* stream, sllm_comm* comm, sllm_load** out);
+
+/* Block until every chunk (and fan-out round) has landed and been verified.  Returns
+ * SLLM_E_CHECKSUM with rep->bad_partition / rep->bad_block naming the first failing
+ * block, or the first CUDA/NCCL error.  Idempotent (returns the same status again).
+ * rep may be NULL. */
+SLLM_API sllm_status sllm_load_wait(sllm_load* load, sllm_load_report* rep);
+
+/* {gpu, device pointer, dtype, shape} of a tensor of this load; valid right after start
+ * (pointers may be set before the data arrives). */
+typedef struct {
+  int32_t gpu;
+  int32_t dtype;
+  int32_t ndim;
+  int32_t reserved;
+  int64_t shape[SLLM_MAX_NDIM];
+  void* ptr;
+  uint64_t nbytes;
+} sllm_tensor_handle;
+SLLM_API sllm_status sllm_load_tensor(const sllm_load* load, const char* name, sllm_tensor_handle* h);
+
+/* Device-computed block checksums of partition p from the last wait (host copy owned by
+ * the load; n_blocks entries; entries of blocks not verified by this process are 0). */
+SLLM_API sllm_status sllm_load_block_checksums(const sllm_load* load, size_t p, const uint64_t** table);
+
+/* Free worker state and scratch; waits for completion first.  Never frees caller memory. */
+SLLM_API void sllm_load_free(sllm_load* load);
+
+/* ------------------------------------------------------------------------------------
+ * Device-resident helpers (the kernels on their own; used for HBM-roofline measurement
+ * and by users who already hold partition bytes in device memory).
+ * ------------------------------------------------------------------------------------ */
+/* Fletcher-64 of every `block`-byte block of a device buffer (len multiple of 16).
+ * out_dev: device pointer to ceil(len/block) uint64.  Asynchronous on `stream`. */
+SLLM_API sllm_status sllm_block_checksums_device(const void* src_dev, uint64_t len, uint64_t block, uint64_t* out_dev,
+                                        int32_t ctas, void* stream);
+/* Scatter partition p, already resident at src_dev (device pointer, L_p bytes), into the
+ * per-tensor buffers dst_tensor[i] (as in sllm_load_start), verifying every block against
+ * the index.  Synchronous; SLLM_E_CHECKSUM names the first bad block in *bad_block. */
+SLLM_API sllm_status sllm_materialise_device(const sllm_index* index, size_t p, const void* src_dev,
+                                    void* const* dst_tensor, int32_t ctas, void* stream, uint64_t* bad_block);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLLM_H_ */

@@ -1,0 +1,439 @@
+"""Python surface of the loader (SURVEY §8(b) "Python surface").  Argument marshalling
+only: every byte the load path moves is moved by libsllm.so (copy engine or its sm_100a
+kernels).  PyTorch provides device memory, streams and the process group.
+
+    idx = Index.open("ckpt/index.bin")                       # S:52 read_index
+    src = {p: HostBuffer.read_partition("ckpt", idx, p) ...}  # file -> pinned DRAM tier
+    res = load(idx, src, gpus={0: 0}, config=LoadConfig())   # P:549 load + P:727 sync
+    res.tensors["model.layers.0.mlp.up_proj.weight"]          # torch view, base + offset
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Dict, Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _abi
+from ._abi import check, lib
+
+_TORCH_DTYPE = None
+
+
+def _torch_dtypes():
+    global _TORCH_DTYPE
+    if _TORCH_DTYPE is None:
+        import torch
+        _TORCH_DTYPE = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32, "i8": torch.int8,
+                        "u8": torch.uint8, "i64": torch.int64}
+    return _TORCH_DTYPE
+
+
+WIDTH = {"f16": 2, "bf16": 2, "f32": 4, "i8": 1, "u8": 1, "i64": 8}
+
+
+@dataclass(frozen=True)
+class TensorInfo:
+    name: str
+    device: int
+    partition: int
+    dtype: str
+    shape: Tuple[int, ...]
+    offset: int
+    nbytes: int
+
+
+@dataclass(frozen=True)
+class PartitionInfo:
+    device: int
+    length: int
+    n_blocks: int
+    n_tensors: int
+
+
+def _src_array(tensors: Sequence) -> Tuple[C.Array, list]:
+    """tensors: (name, device, dtype, shape[, data_ptr, nbytes]) -> SrcTensor[] (+ keepalive)."""
+    arr = (_abi.SrcTensor * max(len(tensors), 1))()
+    keep = []
+    for i, t in enumerate(tensors):
+        name, dev, dt, shape = t[0], t[1], t[2], tuple(int(s) for s in t[3])
+        nm = name.encode("utf-8")
+        shp = (C.c_int64 * max(len(shape), 1))(*shape)
+        keep += [nm, shp]
+        nbytes = math.prod(shape) * WIDTH[dt] if len(t) < 6 else int(t[5])
+        arr[i] = _abi.SrcTensor(nm, int(dev), _abi.DTYPE_CODE[dt], len(shape), shp,
+                                C.c_void_p(int(t[4])) if len(t) > 4 and t[4] else None, nbytes)
+    return arr, keep
+
+
+def _ptr_array(ptrs: Iterable[Optional[int]]) -> C.Array:
+    ptrs = list(ptrs)
+    return (C.c_void_p * max(len(ptrs), 1))(*[C.c_void_p(int(p)) if p else None for p in ptrs])
+
+
+class Index:
+    """Owned handle to a parsed or planned index (sllm_index*)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        self._tensors: Optional[List[TensorInfo]] = None
+        self._by_name: Optional[Dict[str, int]] = None
+
+    # -- constructors ------------------------------------------------------------------
+    @classmethod
+    def plan(cls, tensors: Sequence, align: int = 4096, block: int = 1 << 20, model_id: str = "") -> "Index":
+        """Layout only.  tensors: (name, device, dtype, shape)."""
+        arr, keep = _src_array(tensors)
+        out = C.c_void_p()
+        check(lib().sllm_plan(arr, len(tensors), align, block, model_id.encode(), C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def open(cls, path: str) -> "Index":
+        out = C.c_void_p()
+        check(lib().sllm_index_open(path.encode(), C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def from_bytes(cls, blob: bytes) -> "Index":
+        buf = C.create_string_buffer(bytes(blob), len(blob))
+        out = C.c_void_p()
+        check(lib().sllm_index_from_memory(buf, len(blob), C.byref(out)))
+        return cls(out.value)
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            lib().sllm_index_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    # -- filling -----------------------------------------------------------------------
+    def seal(self, part_ptrs: Sequence[int]) -> None:
+        check(lib().sllm_index_seal(self._h, _ptr_array(part_ptrs)))
+
+    def convert_into(self, tensors: Sequence, part_ptrs: Sequence[int]) -> None:
+        """tensors: (name, device, dtype, shape, data_ptr) in plan order."""
+        arr, keep = _src_array(tensors)
+        check(lib().sllm_convert_into(arr, len(tensors), self._h, _ptr_array(part_ptrs)))
+
+    def serialize(self) -> bytes:
+        n = C.c_size_t()
+        check(lib().sllm_index_serialize(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().sllm_index_serialize(self._h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    # -- queries -----------------------------------------------------------------------
+    def info(self) -> dict:
+        i = _abi.IndexInfo()
+        check(lib().sllm_index_get_info(self._h, C.byref(i)))
+        return {"align": i.align, "block": i.block, "payload_bytes": i.payload_bytes,
+                "n_partitions": i.n_partitions, "n_tensors": i.n_tensors, "model_id": i.model_id.decode()}
+
+    @property
+    def partitions(self) -> List[PartitionInfo]:
+        out = []
+        for p in range(self.info()["n_partitions"]):
+            d, L, nb, nt = C.c_int32(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+            check(lib().sllm_index_partition(self._h, p, C.byref(d), C.byref(L), C.byref(nb), C.byref(nt)))
+            out.append(PartitionInfo(d.value, L.value, nb.value, nt.value))
+        return out
+
+    @property
+    def tensors(self) -> List[TensorInfo]:
+        if self._tensors is None:
+            out = []
+            for i in range(self.info()["n_tensors"]):
+                t = _abi.TensorInfo()
+                check(lib().sllm_index_tensor(self._h, i, C.byref(t)))
+                out.append(TensorInfo(t.name.decode("utf-8"), t.device_id, t.partition, _abi.DTYPE_NAME[t.dtype],
+                                      tuple(t.shape[:t.ndim]), t.offset, t.nbytes))
+            self._tensors = out
+            self._by_name = {t.name: i for i, t in enumerate(out)}
+        return self._tensors
+
+    def find(self, name: str) -> int:
+        i = C.c_size_t()
+        check(lib().sllm_index_find(self._h, name.encode("utf-8"), C.byref(i)))
+        return i.value
+
+    def address(self, name: str, bases: Sequence[int]) -> Tuple[int, int]:
+        """P:549 base + offset; bases[p] = base address of partition p."""
+        arr = (C.c_uint64 * max(len(bases), 1))(*bases)
+        d, a = C.c_int32(), C.c_uint64()
+        check(lib().sllm_tensor_address(self._h, name.encode("utf-8"), arr, C.byref(d), C.byref(a)))
+        return d.value, a.value
+
+    def block_checksums(self, p: int) -> np.ndarray:
+        t = C.POINTER(C.c_uint64)()
+        check(lib().sllm_index_block_checksums(self._h, p, C.byref(t)))
+        n = self.partitions[p].n_blocks
+        return np.ctypeslib.as_array(t, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
+
+
+def convert(tensors: Sequence, out_dir: str, align: int = 4096, block: int = 1 << 20, model_id: str = "") -> None:
+    """SPEC S:43 convert() to <out_dir>/part_<d>.bin + index.bin.  tensors:
+    (name, device, dtype, shape, data_ptr) with host pointers."""
+    arr, keep = _src_array(tensors)
+    check(lib().sllm_convert(arr, len(tensors), align, block, model_id.encode(), out_dir.encode()))
+
+
+def fletcher64(data) -> int:
+    a = np.ascontiguousarray(np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8)) \
+        if not isinstance(data, np.ndarray) else np.ascontiguousarray(data.reshape(-1).view(np.uint8))
+    out = C.c_uint64()
+    check(lib().sllm_fletcher64_host(C.c_void_p(a.ctypes.data), a.size, C.byref(out)))
+    return out.value
+
+
+def chunk_count(length: int, chunk: int) -> int:
+    out = C.c_uint64()
+    check(lib().sllm_chunk_count(length, chunk, C.byref(out)))
+    return out.value
+
+
+def replica_slices(length: int, chunk: int, nranks: int) -> List[Tuple[int, int]]:
+    arr = (C.c_uint64 * (2 * nranks))()
+    check(lib().sllm_replica_slices(length, chunk, nranks, arr))
+    return [(arr[2 * r], arr[2 * r + 1]) for r in range(nranks)]
+
+
+class HostBuffer:
+    """Pinned, device-mapped host memory from sllm_host_alloc (the DRAM tier)."""
+
+    def __init__(self, nbytes: int, gpu: int = -1):
+        p = C.c_void_p()
+        check(lib().sllm_host_alloc(int(nbytes), gpu, C.byref(p)))
+        self.ptr = p.value
+        self.nbytes = int(nbytes)
+
+    @classmethod
+    def read_partition(cls, directory: str, index: Index, p: int, gpu: int = -1, threads: int = 0) -> "HostBuffer":
+        buf = cls(index.partitions[p].length, gpu)
+        check(lib().sllm_host_read_partition(directory.encode(), index.handle, p, C.c_void_p(buf.ptr), threads))
+        return buf
+
+    def numpy(self) -> np.ndarray:
+        return np.ctypeslib.as_array((C.c_uint8 * self.nbytes).from_address(self.ptr))
+
+    def torch(self):
+        import torch
+        return torch.from_numpy(self.numpy())
+
+    def free(self) -> None:
+        if self.ptr:
+            lib().sllm_host_free(C.c_void_p(self.ptr))
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+@dataclass
+class LoadConfig:
+    chunk_bytes: int = 16 << 20   # P:1279 "16MB" (read as MiB, Q9)
+    n_streams: int = 2
+    mode: str = "ce"              # ce | zerocopy | scatter_ce | scatter_zc
+    fanout: str = "none"          # none | bcast
+    verify: bool = True
+    ctas: int = 0
+    profile: bool = False         # per-launch CUDA-event timing (bench roofline)
+
+    def to_c(self) -> _abi.LoadConfig:
+        modes = {"ce": _abi.MODE_CE, "zerocopy": _abi.MODE_ZEROCOPY, "scatter_ce": _abi.MODE_SCATTER_CE,
+                 "scatter_zc": _abi.MODE_SCATTER_ZC}
+        fan = {"none": _abi.FANOUT_NONE, "bcast": _abi.FANOUT_BCAST}
+        return _abi.LoadConfig(self.chunk_bytes, self.n_streams, modes[self.mode], fan[self.fanout],
+                               int(self.verify), self.ctas, int(self.profile))
+
+    @property
+    def scatter(self) -> bool:
+        return self.mode.startswith("scatter")
+
+
+class Comm:
+    """NCCL communicator for the replicated fan-out (sllm_comm*)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().sllm_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def init_rank(cls, uid: bytes, nranks: int, rank: int, gpu: int) -> "Comm":
+        buf = C.create_string_buffer(bytes(uid), 128)
+        out = C.c_void_p()
+        check(lib().sllm_comm_init_rank(buf, nranks, rank, gpu, C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def from_process_group(cls, gpu: int, group=None) -> "Comm":
+        """Build the communicator over a torch.distributed group (id exchanged through it)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls.init_rank(obj[0], world, rank, gpu)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h and self._h.value:
+            lib().sllm_comm_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class LoadResult:
+    """An in-flight or finished load.  ``tensors`` are usable as addresses immediately
+     and hold the checkpoint's bytes once ``wait()`` returned (Q17)."""
+
+    def __init__(self, handle, index: Index, tensors: Dict[str, object], keep: list):
+        self._h = handle
+        self.index = index
+        self.tensors = tensors
+        self._keep = keep
+        self.report: Optional[dict] = None
+
+    def wait(self) -> dict:
+        rep = _abi.LoadReport()
+        st = lib().sllm_load_wait(self._h, C.byref(rep))
+        self.report = rep.as_dict()
+        check(st)
+        return self.report
+
+    def block_checksums(self, p: int) -> np.ndarray:
+        t = C.POINTER(C.c_uint64)()
+        check(lib().sllm_load_block_checksums(self._h, p, C.byref(t)))
+        n = self.index.partitions[p].n_blocks
+        return np.ctypeslib.as_array(t, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
+
+    def handle_of(self, name: str) -> dict:
+        h = _abi.TensorHandle()
+        check(lib().sllm_load_tensor(self._h, name.encode("utf-8"), C.byref(h)))
+        return {"gpu": h.gpu, "ptr": h.ptr, "dtype": _abi.DTYPE_NAME[h.dtype], "shape": tuple(h.shape[:h.ndim]),
+                "nbytes": h.nbytes}
+
+    def free(self):
+        if self._h is not None and self._h.value:
+            lib().sllm_load_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def allocate(index: Index, gpus: Dict[int, int], scatter: bool = False, partitions: Optional[Iterable[int]] = None):
+    """Destination memory through PyTorch's allocator: one uint8 base of L_p bytes per
+    partition (contiguous) or one tensor per index entry (scatter)."""
+    import torch
+    parts = index.partitions
+    sel = sorted(gpus) if partitions is None else sorted(partitions)
+    bases: Dict[int, object] = {}
+    per_tensor: Dict[str, object] = {}
+    tdt = _torch_dtypes()
+    if not scatter:
+        for p in sel:
+            bases[p] = torch.empty(parts[p].length, dtype=torch.uint8, device=f"cuda:{gpus[p]}")
+    else:
+        for t in index.tensors:
+            if t.partition in sel:
+                per_tensor[t.name] = torch.empty(t.shape, dtype=tdt[t.dtype], device=f"cuda:{gpus[t.partition]}")
+    return bases, per_tensor
+
+
+def load_start(index: Index, sources: Dict[int, object], gpus: Dict[int, int], config: Optional[LoadConfig] = None,
+               bases: Optional[Dict[int, object]] = None, per_tensor: Optional[Dict[str, object]] = None,
+               streams: Optional[Dict[int, object]] = None, comm: Optional[Comm] = None) -> LoadResult:
+    """sllm_load_start over preallocated destinations.  sources[p]: HostBuffer or an int
+    host pointer (pinned); gpus[p]: CUDA ordinal; bases[p]: torch uint8 tensor (contiguous)
+    or per_tensor[name]: torch tensor (scatter)."""
+    import torch
+    cfg = config or LoadConfig()
+    parts = index.partitions
+    n = len(parts)
+    src = [None] * n
+    gpu = (C.c_int32 * max(n, 1))()
+    for p, s in sources.items():
+        src[p] = s.ptr if isinstance(s, HostBuffer) else int(s)
+        gpu[p] = int(gpus[p])
+    dst_base = None
+    dst_tensor = None
+    tensors: Dict[str, object] = {}
+    tdt = _torch_dtypes()
+    infos = index.tensors
+    if not cfg.scatter:
+        dst_base = _ptr_array([bases[p].data_ptr() if p in (bases or {}) else None for p in range(n)])
+        for t in infos:
+            if t.partition in sources:
+                b = bases[t.partition]
+                tensors[t.name] = b[t.offset:t.offset + t.nbytes].view(tdt[t.dtype]).view(t.shape)
+    else:
+        dst_tensor = _ptr_array([per_tensor[t.name].data_ptr() if t.partition in sources else None for t in infos])
+        for t in infos:
+            if t.partition in sources:
+                tensors[t.name] = per_tensor[t.name]
+    st = None
+    if streams:
+        st = _ptr_array([streams[p].cuda_stream if p in streams else None for p in range(n)])
+    out = C.c_void_p()
+    ccfg = cfg.to_c()
+    check(lib().sllm_load_start(index.handle, C.byref(ccfg), _ptr_array(src), gpu, dst_base, dst_tensor, st,
+                                comm.handle if comm else None, C.byref(out)))
+    return LoadResult(out, index, tensors, [dst_base, dst_tensor, st, bases, per_tensor, sources])
+
+
+def load(index: Index, sources: Dict[int, object], gpus: Dict[int, int], config: Optional[LoadConfig] = None,
+         wait: bool = True, comm: Optional[Comm] = None, stream_of_caller: bool = True) -> LoadResult:
+    """Allocate destinations with torch, start the load and (by default) wait for it --
+    the whole "time-to-loaded-model" path (Q19)."""
+    import torch
+    cfg = config or LoadConfig()
+    bases, per_tensor = allocate(index, gpus, cfg.scatter, partitions=sources.keys())
+    streams = {p: torch.cuda.current_stream(gpus[p]) for p in sources} if stream_of_caller else None
+    res = load_start(index, sources, gpus, cfg, bases, per_tensor, streams, comm)
+    if wait:
+        res.wait()
+    return res
+
+
+def block_checksums_device(src_ptr: int, length: int, block: int, out_ptr: int, ctas: int = 0, stream=None) -> None:
+    check(lib().sllm_block_checksums_device(C.c_void_p(src_ptr), length, block, C.c_void_p(out_ptr), ctas,
+                                            C.c_void_p(stream.cuda_stream if stream is not None else 0)))
+
+
+def materialise_device(index: Index, p: int, src_ptr: int, per_tensor: Dict[str, object], ctas: int = 0,
+                       stream=None) -> None:
+    infos = index.tensors
+    arr = _ptr_array([per_tensor[t.name].data_ptr() if t.partition == p else None for t in infos])
+    bad = C.c_uint64()
+    check(lib().sllm_materialise_device(index.handle, p, C.c_void_p(src_ptr), arr, ctas,
+                                        C.c_void_p(stream.cuda_stream if stream is not None else 0), C.byref(bad)))

@@ -1,0 +1,104 @@
+// Device-resident entry points of the kernels (K4 checksum, K3 scatter) for partitions
+// already in HBM -- also how bench.py measures them standalone against the HBM roofline.
+#include <algorithm>
+
+#include "runtime.hpp"
+
+namespace sllm {
+
+static int default_grid() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;  // one resident 256-thread CTA per SM (145-152 registers per thread)
+}
+
+void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint64_t* out, int ctas,
+                            cudaStream_t st) {
+  if (!src || !out || !block) fail(SLLM_E_INVALID, "null argument");
+  if (len % 16) fail(SLLM_E_INVALID, "length must be a multiple of 16");
+  if (!is_pow2(block) || block < 16) fail(SLLM_E_INVALID, "block must be a power of two >= 16");
+  if (len == 0) return;
+  const uint64_t nb = ceil_div(len, block);
+  const uint32_t tile = (uint32_t)std::min<uint64_t>(kTile, block);
+  void* scratch = nullptr;
+  const size_t acc_bytes = align_up(nb * sizeof(BlockAcc), 256);
+  SLLM_CUDA(cudaMallocAsync(&scratch, acc_bytes + 256 + 256, st));
+  uint8_t* b = static_cast<uint8_t*>(scratch);
+  Seg* seg = reinterpret_cast<Seg*>(b + acc_bytes);
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(b + acc_bytes + 128);
+  Seg h{0, len, nullptr, 0};
+  SLLM_CUDA(cudaMemsetAsync(b, 0, acc_bytes, st));
+  SLLM_CUDA(cudaMemcpyAsync(seg, &h, sizeof h, cudaMemcpyHostToDevice, st));
+  MatParams mp{};
+  mp.src = static_cast<const uint8_t*>(src);
+  mp.lo = 0;
+  mp.hi = len;
+  mp.segs = seg;
+  mp.seg_begin = 0;
+  mp.seg_end = 1;
+  mp.tile = tile;
+  mp.block = block;
+  mp.part_len = len;
+  mp.acc = reinterpret_cast<BlockAcc*>(b);
+  mp.cs_out = out;
+  mp.bad = bad;
+  SLLM_CUDA(launch_materialise(mp, MatKind::kChecksumOnly, ctas > 0 ? ctas : default_grid(), st));
+  SLLM_CUDA(cudaFreeAsync(scratch, st));
+}
+
+uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, void* const* dst_tensor, int ctas,
+                            cudaStream_t st) {
+  if (!idx || !src || !dst_tensor) fail(SLLM_E_INVALID, "null argument");
+  if (p >= idx->parts.size()) fail(SLLM_E_LOOKUP, "partition index out of range");
+  const PartRec& pr = idx->parts[p];
+  std::vector<Seg> segs;
+  uint64_t cur = 0;
+  for (uint32_t ti : pr.by_offset) {
+    const TensorRec& t = idx->tensors[ti];
+    if (!dst_tensor[ti] || (reinterpret_cast<uintptr_t>(dst_tensor[ti]) & 15))
+      fail(SLLM_E_INVALID, "destination of '" + t.name + "' is null or not 16-byte aligned");
+    if (t.offset > cur) segs.push_back(Seg{cur, t.offset - cur, nullptr, 0});
+    uint64_t end16 = align_up(t.offset + t.nbytes, 16);
+    segs.push_back(Seg{t.offset, end16 - t.offset, static_cast<uint8_t*>(dst_tensor[ti]), t.nbytes});
+    cur = end16;
+  }
+  if (pr.length > cur) segs.push_back(Seg{cur, pr.length - cur, nullptr, 0});
+  const uint64_t nb = std::max<uint64_t>(pr.n_blocks, 1);
+  const size_t seg_bytes = align_up(segs.size() * sizeof(Seg), 256);
+  const size_t acc_bytes = align_up(nb * sizeof(BlockAcc), 256);
+  const size_t tab = align_up(nb * 8, 256);
+  void* scratch = nullptr;
+  SLLM_CUDA(cudaMallocAsync(&scratch, seg_bytes + acc_bytes + tab + 256, st));
+  uint8_t* b = static_cast<uint8_t*>(scratch);
+  Seg* d_segs = reinterpret_cast<Seg*>(b);
+  BlockAcc* d_acc = reinterpret_cast<BlockAcc*>(b + seg_bytes);
+  uint64_t* d_expect = reinterpret_cast<uint64_t*>(b + seg_bytes + acc_bytes);
+  unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(b + seg_bytes + acc_bytes + tab);
+  SLLM_CUDA(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice, st));
+  SLLM_CUDA(cudaMemsetAsync(d_acc, 0, acc_bytes, st));
+  SLLM_CUDA(cudaMemsetAsync(d_bad, 0xFF, 8, st));
+  const bool check = idx->block != 0;
+  if (check) SLLM_CUDA(cudaMemcpyAsync(d_expect, pr.checksums.data(), pr.n_blocks * 8, cudaMemcpyHostToDevice, st));
+  MatParams mp{};
+  mp.src = static_cast<const uint8_t*>(src);
+  mp.lo = 0;
+  mp.hi = pr.length;
+  mp.segs = d_segs;
+  mp.seg_begin = 0;
+  mp.seg_end = (uint32_t)segs.size();
+  mp.tile = idx->block ? (uint32_t)std::min<uint64_t>(kTile, idx->block) : kTile;
+  mp.block = idx->block ? idx->block : kTile;
+  mp.part_len = pr.length;
+  mp.acc = d_acc;
+  mp.expect = check ? d_expect : nullptr;
+  mp.bad = d_bad;
+  SLLM_CUDA(launch_materialise(mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas > 0 ? ctas : default_grid(), st));
+  unsigned long long bad = ~0ull;
+  SLLM_CUDA(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st));
+  SLLM_CUDA(cudaStreamSynchronize(st));
+  SLLM_CUDA(cudaFreeAsync(scratch, st));
+  return bad;
+}
+
+}  // namespace sllm

@@ -1,0 +1,192 @@
+// sm_100a kernels of the load path:
+//   K2  zero-copy read of host-mapped pinned memory (PCIe, SM-issued 16 B loads) -> HBM,
+//       with the block checksum fused;
+//   K3  index-driven scatter: partition bytes (staging chunk in HBM, or host-mapped) ->
+//       per-tensor buffers, checksum fused;
+//   K4  checksum-only pass over a device buffer (CE-contiguous mode verification).
+// All three are one template: a persistent grid walks fixed-size tiles of the launch's
+// byte range; inside a tile it walks the index-derived segments (tensor bytes or
+// padding) with coalesced 16-byte vectors, U loads in flight per thread.
+//
+// Checksum (Q8): Fletcher-64 per block of B bytes,
+// evaluated in closed form so tiles/threads may add their terms in any order:
+//   s1 = sum_i w_i,  s2 = sum_i (n - i) w_i = n*sum w - sum_v i0_v*sum4_v - sum_v (w1+2w2+3w3)_v
+// (v = 16-byte vector whose first word has block index i0_v).  Per-thread partials are
+// folded mod 2^32-1 after every segment, reduced over the CTA with warp shuffles, and
+// added atomically into the block's accumulator; the CTA finishing a block's last tile
+// finalises it and compares against the index's table.
+#include "kernels.cuh"
+
+namespace sllm {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 16;                       // 16 x 16 B in flight per thread
+constexpr unsigned long long kM = 0xFFFFFFFFull;  // 2^32 - 1
+
+__device__ __forceinline__ unsigned long long fold(unsigned long long x) {
+  x = (x & kM) + (x >> 32);
+  x = (x & kM) + (x >> 32);
+  return x >= kM ? x - kM : x;
+}
+
+template <bool kHostSrc>
+__device__ __forceinline__ uint4 load16(const uint8_t* p) {
+  uint4 r;
+  if (kHostSrc) {
+    // host-mapped pinned memory over PCIe: plain global load, no L1 allocation
+    asm("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  } else {
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  }
+  return r;
+}
+
+__device__ __forceinline__ void store16(uint8_t* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// Store the first n (< 16) bytes of v at p (tensor tail; the rest of the vector is padding).
+__device__ __forceinline__ void store_partial(uint8_t* p, const uint4& v, uint32_t n) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (uint32_t k = 0; k < 16; ++k)
+    if (k < n) p[k] = (uint8_t)(w[k / 4] >> (8 * (k % 4)));
+}
+
+template <bool kStore, bool kCheck, bool kHostSrc>
+__global__ void __launch_bounds__(kThreads) materialise_kernel(const MatParams p) {
+  __shared__ uint32_t s_seg;
+  __shared__ unsigned long long s_red[3][kThreads / 32];
+  const int tid = threadIdx.x;
+  const uint64_t T = p.tile;
+  const uint64_t ntiles = (p.hi - p.lo + T - 1) / T;
+
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t t_lo = p.lo + t * T;
+    const uint64_t t_hi = min(t_lo + T, p.hi);
+    if (tid == 0) {  // last segment with off <= t_lo
+      uint32_t lo = p.seg_begin, hi = p.seg_end;
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (p.segs[mid].off <= t_lo) lo = mid; else hi = mid;
+      }
+      s_seg = lo;
+    }
+    __syncthreads();
+    const uint32_t first = s_seg;
+    const uint64_t blk_lo = kCheck ? (t_lo / p.block) * p.block : 0;
+    unsigned long long a = 0, b = 0, c = 0;
+
+    for (uint32_t s = first; s < p.seg_end; ++s) {
+      const Seg sg = p.segs[s];
+      if (sg.off >= t_hi) break;
+      const uint64_t x_lo = max(sg.off, t_lo);
+      const uint64_t x_hi = min(sg.off + sg.len, t_hi);
+      for (uint64_t x0 = x_lo + (uint64_t)tid * 16; x0 < x_hi; x0 += (uint64_t)kThreads * 16 * kUnroll) {
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint64_t x = x0 + (uint64_t)u * kThreads * 16;
+          if (x < x_hi) v[u] = load16<kHostSrc>(p.src + (x - p.src_origin));
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint64_t x = x0 + (uint64_t)u * kThreads * 16;
+          if (x < x_hi) {
+            if (kStore && sg.dst) {
+              const uint64_t rel = x - sg.off;
+              if (rel + 16 <= sg.valid) store16(sg.dst + rel, v[u]);
+              else if (rel < sg.valid) store_partial(sg.dst + rel, v[u], (uint32_t)(sg.valid - rel));
+            }
+            if (kCheck) {
+              const uint32_t i0 = (uint32_t)((x - blk_lo) >> 2);
+              const unsigned long long s4 = (unsigned long long)v[u].x + v[u].y + v[u].z + v[u].w;
+              a += s4;
+              b += (unsigned long long)i0 * s4;
+              c += (unsigned long long)v[u].y + 2ull * v[u].z + 3ull * v[u].w;
+            }
+          }
+        }
+      }
+      if (kCheck) {  // keep partials < 2^32 whatever the number of segments per tile
+        a = fold(a);
+        b = fold(b);
+        c = fold(c);
+      }
+    }
+
+    if (kCheck) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+      }
+      if ((tid & 31) == 0) {
+        s_red[0][tid >> 5] = a;
+        s_red[1][tid >> 5] = b;
+        s_red[2][tid >> 5] = c;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long A = 0, Bs = 0, C = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+          A += s_red[0][w];
+          Bs += s_red[1][w];
+          C += s_red[2][w];
+        }
+        const uint64_t j = t_lo / p.block;
+        BlockAcc* acc = p.acc + j;
+        atomicAdd(&acc->a, fold(A));
+        atomicAdd(&acc->b, fold(Bs));
+        atomicAdd(&acc->c, fold(C));
+        __threadfence();
+        const uint64_t blen = min(p.block, p.part_len - j * p.block);
+        const unsigned long long tiles_in_block = (blen + T - 1) / T;
+        if (atomicAdd(&acc->tiles_done, 1ull) == tiles_in_block - 1) {
+          __threadfence();
+          const unsigned long long fa = fold(atomicAdd(&acc->a, 0ull));
+          const unsigned long long fb = fold(atomicAdd(&acc->b, 0ull));
+          const unsigned long long fc = fold(atomicAdd(&acc->c, 0ull));
+          const unsigned long long n = (blen >> 2) % kM;
+          const unsigned long long s2 = fold(fold(n * fa) + (kM - fb) + (kM - fc));
+          const unsigned long long cs = (s2 << 32) | fa;
+          if (p.cs_out) p.cs_out[j] = cs;
+          if (p.expect && p.expect[j] != cs) atomicMin(p.bad, (unsigned long long)j);
+        }
+      }
+    }
+    __syncthreads();  // s_seg / s_red reuse by the next tile
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream) {
+  if (p.hi <= p.lo) return cudaSuccess;
+  if (grid < 1) grid = 1;
+  const uint64_t ntiles = (p.hi - p.lo + p.tile - 1) / p.tile;
+  if ((uint64_t)grid > ntiles) grid = (int)ntiles;
+  switch (kind) {
+    case MatKind::kChecksumOnly:
+      if (p.host_src) materialise_kernel<false, true, true><<<grid, kThreads, 0, stream>>>(p);
+      else materialise_kernel<false, true, false><<<grid, kThreads, 0, stream>>>(p);
+      break;
+    case MatKind::kCopyChecksum:
+      if (p.host_src) materialise_kernel<true, true, true><<<grid, kThreads, 0, stream>>>(p);
+      else materialise_kernel<true, true, false><<<grid, kThreads, 0, stream>>>(p);
+      break;
+    case MatKind::kCopyOnly:
+      if (p.host_src) materialise_kernel<true, false, true><<<grid, kThreads, 0, stream>>>(p);
+      else materialise_kernel<true, false, false><<<grid, kThreads, 0, stream>>>(p);
+      break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace sllm

@@ -1,0 +1,54 @@
+// Device-side data structures shared by kernels.cu (device code) and loader.cpp (host).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sllm {
+
+// A 16-byte aligned byte range of a partition and where its bytes go.
+//   [off, off+len)  partition bytes covered (off, len multiples of 16)
+//   dst             device pointer receiving byte `off` (nullptr: checksum only -- padding)
+//   valid           bytes of [off, off+valid) that belong to the tensor (<= len); the rest
+//                   of the last 16-byte vector is partition padding and is not stored.
+struct Seg {
+  uint64_t off;
+  uint64_t len;
+  uint8_t* dst;
+  uint64_t valid;
+};
+
+// Per-block checksum accumulator (closed form of Q8):
+//   a = sum w_i,  b = sum i*w_i (i = word index in the block, per 16 B vector i0*sum4),
+//   c = sum k*w_{i0+k} within each vector;  s1 = a,  s2 = n*a - b - c  (all mod 2^32-1).
+struct BlockAcc {
+  unsigned long long a, b, c, tiles_done;
+};
+
+// One launch of the materialise/checksum kernel covers partition bytes [lo, hi).
+struct MatParams {
+  const uint8_t* src;        // address holding partition byte `src_origin` (host-mapped or device)
+  uint64_t src_origin;
+  uint64_t lo, hi;           // multiples of 16; lo is a multiple of `tile`
+  const Seg* segs;           // segments covering [lo, hi), sorted by off
+  uint32_t seg_begin, seg_end;
+  uint32_t tile;             // bytes per work tile (divides block; multiple of 16)
+  uint64_t block;            // checksum block size B (0 = no checksum)
+  uint64_t part_len;         // L_p
+  BlockAcc* acc;             // n_blocks accumulators (zeroed before the load)
+  const uint64_t* expect;    // expected block checksums, or nullptr
+  uint64_t* cs_out;          // computed block checksums, or nullptr
+  unsigned long long* bad;   // min failing block index (init UINT64_MAX)
+  int host_src;              // 1: src is host-mapped pinned memory (zero-copy over PCIe)
+};
+
+enum class MatKind : int {
+  kChecksumOnly = 0,   // K4: read a device buffer, checksum only
+  kCopyChecksum = 1,   // K2/K3: read (host-mapped or device), store per segment, checksum
+  kCopyOnly = 2        // K2/K3 with verify off
+};
+
+// Launch on `stream` with `grid` CTAs (grid-stride over tiles).  Returns cudaGetLastError().
+cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream);
+
+}  // namespace sllm

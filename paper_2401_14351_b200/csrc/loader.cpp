@@ -1,0 +1,591 @@
+// The load path: one host worker thread per partition drives a chunk pipeline on a
+// few CUDA streams of its GPU.
+//
+//   PAPER.md P:576-602 (§Multi-Tier Loading Subsystem): chunk-based data management,
+//   "parallel DRAM-to-GPU PCIe links", pinned memory ("one thread is enough" P:692),
+//   a task-queue pipeline of (offset, size) chunk indices;
+//   "divides each partition into chunks with equal size (except for the last one)";
+//   tensors are base + offset; sync returns when all data is loaded.
+//
+// On B200 the task queue between the DRAM tier and the GPU is the CUDA stream itself:
+// chunk k is issued on stream k mod S (copy-engine DMA or a zero-copy kernel), its
+// verification/scatter kernel follows on the same stream, and the next chunk's transfer
+// proceeds on the other stream(s) -- the pipeline "avoids synchronization for all data
+// on each storage tier" without host round trips.
+#include <algorithm>
+#include <set>
+
+#include "runtime.hpp"
+
+namespace sllm {
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what) {
+  fail(SLLM_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------------------------
+// Device contexts
+// ------------------------------------------------------------------------------------
+static std::mutex g_ctx_mu;
+static std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
+
+DeviceCtx& device_ctx(int dev) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  if (dev < 0) fail(SLLM_E_INVALID, "negative GPU ordinal");
+  if ((size_t)dev >= g_ctx.size()) g_ctx.resize(dev + 1);
+  if (!g_ctx[dev]) {
+    g_ctx[dev].reset(new DeviceCtx);
+    g_ctx[dev]->dev = dev;
+  }
+  return *g_ctx[dev];
+}
+
+void DeviceCtx::ensure(int n) {
+  for (int s = 0; s < n; ++s)
+    if (!streams[s]) SLLM_CUDA(cudaStreamCreateWithFlags(&streams[s], cudaStreamNonBlocking));
+  if (!comm_stream) SLLM_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+}
+
+void DeviceCtx::ensure_staging(int n, uint64_t bytes) {
+  if (bytes > staging_bytes) {
+    for (auto& p : staging)
+      if (p) { SLLM_CUDA(cudaFree(p)); p = nullptr; }
+    staging_bytes = bytes;
+  }
+  for (int s = 0; s < n; ++s)
+    if (!staging[s]) SLLM_CUDA(cudaMalloc(&staging[s], staging_bytes));
+}
+
+// ------------------------------------------------------------------------------------
+// Busy set (concurrent loads of the same destinations are rejected)
+// ------------------------------------------------------------------------------------
+static std::mutex g_busy_mu;
+static std::set<const void*> g_busy;
+
+// ------------------------------------------------------------------------------------
+// Load objects
+// ------------------------------------------------------------------------------------
+struct PartJob {
+  size_t p = 0;
+  int gpu = 0;
+  const uint8_t* src = nullptr;      // host pointer (pinned)
+  const uint8_t* src_dev = nullptr;  // its device-visible alias (zero-copy modes)
+  uint8_t* dst_base = nullptr;
+  cudaStream_t origin = nullptr;
+  // fan-out slice of this rank (whole partition when not replicated)
+  uint64_t lo = 0, hi = 0;
+  std::vector<Seg> segs;
+  std::vector<uint32_t> chunk_seg;  // first segment of each chunk of [0, L)
+  // device scratch (one cudaMallocAsync block)
+  void* scratch = nullptr;
+  Seg* d_segs = nullptr;
+  BlockAcc* d_acc = nullptr;
+  uint64_t* d_expect = nullptr;
+  uint64_t* d_cs = nullptr;
+  unsigned long long* d_bad = nullptr;
+  cudaEvent_t ev[4] = {};  // start, end, setup, origin
+  // results
+  std::vector<uint64_t> h_cs;
+  bool h_cs_valid = false;
+  unsigned long long h_bad = ~0ull;
+  sllm_status status = SLLM_OK;
+  std::string error;
+  uint64_t t_issue_ns = 0;
+  float t_dev_ms = 0.f;
+  uint64_t chunks = 0, launches = 0, copies = 0, transferred = 0, fanout = 0;
+  // profile: (start, end) event pairs around kernel launches / copies
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev, cev;
+  uint64_t kernel_bytes = 0;
+  double kernel_ms = 0, copy_ms = 0;
+  std::thread th;
+};
+
+}  // namespace sllm
+
+struct sllm_load {
+  const sllm_index* idx = nullptr;
+  sllm_load_config cfg{};
+  sllm_comm* comm = nullptr;
+  std::vector<sllm::PartJob> jobs;
+  std::vector<void*> dst_tensor;  // scatter modes: per tensor
+  std::vector<const void*> busy_keys;
+  std::chrono::steady_clock::time_point t0;
+  bool joined = false;
+  sllm_status result = SLLM_OK;
+  sllm_load_report rep{};
+};
+
+namespace sllm {
+
+static uint64_t now_ns() {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Segments of partition p: every tensor [off, align16(off+size)) -> its destination,
+// every gap between tensors (padding) -> checksum only.  Contiguous modes use a single
+// segment [0, L) -> dst_base.
+static void build_segments(const sllm_index& idx, PartJob& j, bool scatter, const std::vector<void*>& dst_tensor,
+                           uint64_t chunk) {
+  const PartRec& pr = idx.parts[j.p];
+  j.segs.clear();
+  if (!scatter) {
+    j.segs.push_back(Seg{0, pr.length, j.dst_base, pr.length});
+  } else {
+    uint64_t cur = 0;
+    for (uint32_t ti : pr.by_offset) {
+      const TensorRec& t = idx.tensors[ti];
+      if (t.offset > cur) j.segs.push_back(Seg{cur, t.offset - cur, nullptr, 0});
+      uint64_t end16 = align_up(t.offset + t.nbytes, 16);
+      j.segs.push_back(Seg{t.offset, end16 - t.offset, static_cast<uint8_t*>(dst_tensor[ti]), t.nbytes});
+      cur = end16;
+    }
+    if (pr.length > cur) j.segs.push_back(Seg{cur, pr.length - cur, nullptr, 0});
+  }
+  uint64_t nch = ceil_div(pr.length, chunk);
+  j.chunk_seg.assign(nch + 1, 0);
+  size_t s = 0;
+  for (uint64_t k = 0; k < nch; ++k) {
+    uint64_t lo = k * chunk;
+    while (s + 1 < j.segs.size() && j.segs[s + 1].off <= lo) ++s;
+    j.chunk_seg[k] = (uint32_t)s;
+  }
+  j.chunk_seg[nch] = (uint32_t)j.segs.size();
+}
+
+// Work tile: 64 KiB, or the checksum block when smaller (tiles never straddle blocks).
+static uint32_t tile_for(const sllm_index& idx) {
+  return idx.block ? (uint32_t)std::min<uint64_t>(kTile, idx.block) : kTile;
+}
+
+static int default_ctas(int mode) {
+  switch (mode) {
+    case SLLM_MODE_ZEROCOPY: case SLLM_MODE_SCATTER_ZC: return 32;
+    default: return 64;
+  }
+}
+
+static std::pair<cudaEvent_t, cudaEvent_t> timed_begin(bool on, cudaStream_t st) {
+  std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
+  if (!on) return e;
+  SLLM_CUDA(cudaEventCreate(&e.first));
+  SLLM_CUDA(cudaEventCreate(&e.second));
+  SLLM_CUDA(cudaEventRecord(e.first, st));
+  return e;
+}
+
+static void timed_end(std::pair<cudaEvent_t, cudaEvent_t> e, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& out,
+                      cudaStream_t st) {
+  if (!e.first) return;
+  SLLM_CUDA(cudaEventRecord(e.second, st));
+  out.push_back(e);
+}
+
+static void launch(PartJob& j, bool prof, const MatParams& mp, MatKind kind, int ctas, cudaStream_t st) {
+  auto e = timed_begin(prof, st);
+  SLLM_CUDA(launch_materialise(mp, kind, ctas, st));
+  timed_end(e, j.kev, st);
+  if (prof) j.kernel_bytes += mp.hi - mp.lo;
+  j.launches++;
+}
+
+static void copy_h2d(PartJob& j, bool prof, void* dst, const void* src, uint64_t n, cudaStream_t st) {
+  auto e = timed_begin(prof, st);
+  SLLM_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+  timed_end(e, j.cev, st);
+  j.copies++;
+}
+
+// Issue one chunk [lo, hi) of job j on stream st (slot = staging slot for SCATTER_CE).
+static void issue_chunk(const sllm_index& idx, const sllm_load_config& cfg, DeviceCtx& dc, PartJob& j,
+                        uint64_t k, uint64_t lo, uint64_t hi, int slot, cudaStream_t st) {
+  const PartRec& pr = idx.parts[j.p];
+  const bool check = cfg.verify && idx.block;
+  const bool prof = cfg.profile != 0;
+  const int ctas = cfg.ctas > 0 ? cfg.ctas : default_ctas(cfg.mode);
+  MatParams mp{};
+  mp.lo = lo;
+  mp.hi = hi;
+  mp.segs = j.d_segs;
+  mp.seg_begin = j.chunk_seg[k];
+  uint64_t nch = j.chunk_seg.size() - 1;
+  mp.seg_end = k + 1 < nch ? std::min<uint32_t>(j.chunk_seg[k + 1] + 1, (uint32_t)j.segs.size())
+                           : (uint32_t)j.segs.size();
+  mp.tile = tile_for(idx);
+  mp.block = idx.block ? idx.block : kTile;
+  mp.part_len = pr.length;
+  mp.acc = j.d_acc;
+  mp.expect = check ? j.d_expect : nullptr;
+  mp.cs_out = check ? j.d_cs : nullptr;
+  mp.bad = j.d_bad;
+  switch (cfg.mode) {
+    case SLLM_MODE_CE:
+      copy_h2d(j, prof, j.dst_base + lo, j.src + lo, hi - lo, st);
+      if (check) {
+        mp.src = j.dst_base;
+        mp.src_origin = 0;
+        mp.host_src = 0;
+        launch(j, prof, mp, MatKind::kChecksumOnly, ctas, st);
+      }
+      break;
+    case SLLM_MODE_ZEROCOPY:
+    case SLLM_MODE_SCATTER_ZC:
+      mp.src = j.src_dev;
+      mp.src_origin = 0;
+      mp.host_src = 1;
+      launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, st);
+      break;
+    case SLLM_MODE_SCATTER_CE:
+      copy_h2d(j, prof, dc.staging[slot], j.src + lo, hi - lo, st);
+      mp.src = static_cast<const uint8_t*>(dc.staging[slot]);
+      mp.src_origin = lo;
+      mp.host_src = 0;
+      launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, st);
+      break;
+    default:
+      fail(SLLM_E_INVALID, "unknown mode");
+  }
+  j.chunks++;
+  j.transferred += hi - lo;
+}
+
+// Checksum-only verification of bytes that arrived through the fan-out.
+static void verify_range(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, uint64_t lo, uint64_t hi,
+                         cudaStream_t st) {
+  MatParams mp{};
+  mp.src = j.dst_base;
+  mp.lo = lo;
+  mp.hi = hi;
+  mp.segs = j.d_segs;
+  mp.seg_begin = 0;
+  mp.seg_end = 1;  // contiguous single segment
+  mp.tile = tile_for(idx);
+  mp.block = idx.block;
+  mp.part_len = idx.parts[j.p].length;
+  mp.acc = j.d_acc;
+  mp.expect = j.d_expect;
+  mp.cs_out = j.d_cs;
+  mp.bad = j.d_bad;
+  launch(j, cfg.profile != 0, mp, MatKind::kChecksumOnly, cfg.ctas > 0 ? cfg.ctas : 64, st);
+}
+
+static void run_job(sllm_load* L, PartJob& j) {
+  const sllm_index& idx = *L->idx;
+  const sllm_load_config& cfg = L->cfg;
+  const PartRec& pr = idx.parts[j.p];
+  const uint64_t t0 = now_ns();
+  SLLM_CUDA(cudaSetDevice(j.gpu));
+  DeviceCtx& dc = device_ctx(j.gpu);
+  {
+    std::lock_guard<std::mutex> g(dc.mu);
+    dc.ensure(cfg.n_streams);
+    if (cfg.mode == SLLM_MODE_SCATTER_CE) dc.ensure_staging(cfg.n_streams, cfg.chunk_bytes);
+  }
+  cudaStream_t s0 = dc.streams[0];
+  for (auto& e : j.ev) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
+  const uint64_t nb = pr.n_blocks;
+  const size_t seg_bytes = align_up(j.segs.size() * sizeof(Seg), 256);
+  const size_t acc_bytes = align_up(std::max<uint64_t>(nb, 1) * sizeof(BlockAcc), 256);
+  const size_t tab_bytes = align_up(std::max<uint64_t>(nb, 1) * 8, 256);
+  const size_t total = seg_bytes + acc_bytes + 2 * tab_bytes + 256;
+  if (j.origin) {
+    SLLM_CUDA(cudaEventRecord(j.ev[3], j.origin));
+    SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[3], 0));
+  }
+  SLLM_CUDA(cudaMallocAsync(&j.scratch, total, s0));
+  uint8_t* base = static_cast<uint8_t*>(j.scratch);
+  j.d_segs = reinterpret_cast<Seg*>(base);
+  j.d_acc = reinterpret_cast<BlockAcc*>(base + seg_bytes);
+  j.d_expect = reinterpret_cast<uint64_t*>(base + seg_bytes + acc_bytes);
+  j.d_cs = reinterpret_cast<uint64_t*>(base + seg_bytes + acc_bytes + tab_bytes);
+  j.d_bad = reinterpret_cast<unsigned long long*>(base + seg_bytes + acc_bytes + 2 * tab_bytes);
+  SLLM_CUDA(cudaMemcpyAsync(j.d_segs, j.segs.data(), j.segs.size() * sizeof(Seg), cudaMemcpyHostToDevice, s0));
+  SLLM_CUDA(cudaMemsetAsync(j.d_acc, 0, acc_bytes + tab_bytes, s0));  // accumulators (+ expect, overwritten)
+  SLLM_CUDA(cudaMemsetAsync(j.d_cs, 0, tab_bytes, s0));
+  SLLM_CUDA(cudaMemsetAsync(j.d_bad, 0xFF, 8, s0));
+  if (nb) SLLM_CUDA(cudaMemcpyAsync(j.d_expect, pr.checksums.data(), nb * 8, cudaMemcpyHostToDevice, s0));
+  SLLM_CUDA(cudaEventRecord(j.ev[0], s0));
+  SLLM_CUDA(cudaEventRecord(j.ev[2], s0));
+  const int S = cfg.n_streams;
+  for (int s = 1; s < S; ++s) SLLM_CUDA(cudaStreamWaitEvent(dc.streams[s], j.ev[2], 0));
+
+  const uint64_t C = cfg.chunk_bytes;
+  if (cfg.fanout == SLLM_FANOUT_BCAST) {
+    // Replicated load: this rank moves its slice over PCIe; every chunk
+    // round is then broadcast from its owner over NVLink (grouped, one root per slice).
+    const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
+    std::vector<uint64_t> lohi(2 * R);
+    if (sllm_replica_slices(pr.length, C, R, lohi.data()) != SLLM_OK) fail(SLLM_E_INVALID, "slice plan failed");
+    uint64_t rounds = 0;
+    for (int q = 0; q < R; ++q) rounds = std::max(rounds, ceil_div(lohi[2 * q + 1] - lohi[2 * q], C));
+    std::vector<cudaEvent_t> evk(rounds);
+    for (auto& e : evk) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaStream_t cs = dc.comm_stream;
+    SLLM_CUDA(cudaStreamWaitEvent(cs, j.ev[2], 0));
+    for (uint64_t r = 0; r < rounds; ++r) {
+      uint64_t lo = lohi[2 * me] + r * C;
+      if (lo < lohi[2 * me + 1]) {
+        uint64_t hi = std::min(lo + C, lohi[2 * me + 1]);
+        cudaStream_t st = dc.streams[r % S];
+        issue_chunk(idx, cfg, dc, j, lo / C, lo, hi, (int)(r % S), st);
+        SLLM_CUDA(cudaEventRecord(evk[r], st));
+        SLLM_CUDA(cudaStreamWaitEvent(cs, evk[r], 0));
+      }
+      std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
+      for (int q = 0; q < R; ++q) {
+        uint64_t a = lohi[2 * q] + r * C;
+        ranges[q] = a < lohi[2 * q + 1] ? std::pair<uint64_t, uint64_t>(a, std::min(a + C, lohi[2 * q + 1]))
+                                        : std::pair<uint64_t, uint64_t>(0, 0);
+        if (q != me && ranges[q].second > ranges[q].first) j.fanout += ranges[q].second - ranges[q].first;
+      }
+      nccl_bcast_group(L->comm, ranges, j.dst_base, cs);
+      if (cfg.verify && idx.block)
+        for (int q = 0; q < R; ++q)
+          if (q != me && ranges[q].second > ranges[q].first) verify_range(idx, cfg, j, ranges[q].first, ranges[q].second, cs);
+    }
+    SLLM_CUDA(cudaEventRecord(j.ev[2], cs));
+    SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[2], 0));
+    for (auto& e : evk) cudaEventDestroy(e);
+  } else {
+    const uint64_t nch = ceil_div(pr.length, C);
+    for (uint64_t k = 0; k < nch; ++k) {
+      uint64_t lo = k * C, hi = std::min(lo + C, pr.length);
+      issue_chunk(idx, cfg, dc, j, k, lo, hi, (int)(k % S), dc.streams[k % S]);
+    }
+  }
+  // join the streams into s0, then let the caller's stream wait for the load
+  for (int s = 1; s < S; ++s) {
+    cudaEvent_t e;
+    SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SLLM_CUDA(cudaEventRecord(e, dc.streams[s]));
+    SLLM_CUDA(cudaStreamWaitEvent(s0, e, 0));
+    SLLM_CUDA(cudaEventDestroy(e));  // destruction is deferred until the event completes
+  }
+  SLLM_CUDA(cudaEventRecord(j.ev[1], s0));
+  if (j.origin) SLLM_CUDA(cudaStreamWaitEvent(j.origin, j.ev[1], 0));
+  j.t_issue_ns = now_ns() - t0;
+  SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
+  SLLM_CUDA(cudaMemcpy(&j.h_bad, j.d_bad, 8, cudaMemcpyDeviceToHost));
+  SLLM_CUDA(cudaEventElapsedTime(&j.t_dev_ms, j.ev[0], j.ev[1]));
+  for (auto* v : {&j.kev, &j.cev}) {
+    double sum = 0;
+    for (auto& e : *v) {
+      float ms = 0;
+      SLLM_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+      sum += ms;
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    (v == &j.kev ? j.kernel_ms : j.copy_ms) = sum;
+    v->clear();
+  }
+  SLLM_CUDA(cudaGetLastError());
+}
+
+static void run_job_guarded(sllm_load* L, PartJob& j) {
+  try {
+    run_job(L, j);
+  } catch (const Error& e) {
+    j.status = e.code;
+    j.error = e.what();
+  } catch (const std::exception& e) {
+    j.status = SLLM_E_INVALID;
+    j.error = e.what();
+  }
+}
+
+}  // namespace sllm
+
+using namespace sllm;
+
+sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_config* cfg_in, const void* const* host_src,
+                                     const int32_t* gpu, void* const* dst_base, void* const* dst_tensor,
+                                     void* const* stream, sllm_comm* comm) {
+  if (!idx) fail(SLLM_E_INVALID, "null index");
+  if (!idx->sealed) fail(SLLM_E_INVALID, "index is planned but not sealed");
+  sllm_load_config cfg{};
+  if (cfg_in) cfg = *cfg_in;
+  else cfg.verify = 1;
+  if (cfg.chunk_bytes == 0) cfg.chunk_bytes = 16ull << 20;
+  if (cfg.n_streams == 0) cfg.n_streams = 2;
+  if (cfg.n_streams < 1 || cfg.n_streams > kMaxStreams) fail(SLLM_E_INVALID, "n_streams must be in 1..8");
+  if (cfg.mode < SLLM_MODE_CE || cfg.mode > SLLM_MODE_SCATTER_ZC) fail(SLLM_E_INVALID, "unknown mode");
+  if (cfg.profile != 0 && cfg.profile != 1) fail(SLLM_E_INVALID, "profile must be 0 or 1");
+  if (cfg.chunk_bytes % tile_for(*idx)) fail(SLLM_E_INVALID, "chunk size must be a multiple of the 64 KiB work tile");
+  if (idx->block && cfg.chunk_bytes % idx->block) fail(SLLM_E_INVALID, "chunk size must be a multiple of the block size");
+  if (cfg.chunk_bytes % idx->align) fail(SLLM_E_INVALID, "chunk size must be a multiple of the alignment");
+  const bool scatter = cfg.mode == SLLM_MODE_SCATTER_CE || cfg.mode == SLLM_MODE_SCATTER_ZC;
+  if (cfg.fanout == SLLM_FANOUT_BCAST) {
+    if (!comm) fail(SLLM_E_INVALID, "fan-out needs a communicator");
+    if (idx->parts.size() != 1) fail(SLLM_E_INVALID, "fan-out needs a single-partition (replicated) index");
+    if (scatter) fail(SLLM_E_INVALID, "fan-out supports the contiguous modes only");
+  } else if (cfg.fanout != SLLM_FANOUT_NONE) {
+    fail(SLLM_E_INVALID, "unknown fan-out");
+  }
+  if (!host_src || !gpu) fail(SLLM_E_INVALID, "null host_src / gpu array");
+  if (scatter && !dst_tensor) fail(SLLM_E_INVALID, "scatter modes need dst_tensor");
+  if (!scatter && !dst_base) fail(SLLM_E_INVALID, "contiguous modes need dst_base");
+
+  std::unique_ptr<sllm_load> L(new sllm_load);
+  L->idx = idx;
+  L->cfg = cfg;
+  L->comm = comm;
+  L->t0 = std::chrono::steady_clock::now();
+  if (scatter) L->dst_tensor.assign(dst_tensor, dst_tensor + idx->tensors.size());
+  for (size_t p = 0; p < idx->parts.size(); ++p) {
+    if (!host_src[p]) continue;
+    PartJob j;
+    j.p = p;
+    j.gpu = gpu[p];
+    j.src = static_cast<const uint8_t*>(host_src[p]);
+    j.dst_base = dst_base ? static_cast<uint8_t*>(dst_base[p]) : nullptr;
+    j.origin = stream ? static_cast<cudaStream_t>(stream[p]) : nullptr;
+    if (!scatter && !j.dst_base) fail(SLLM_E_INVALID, "null dst_base for a loaded partition");
+    if (cfg.fanout == SLLM_FANOUT_BCAST && comm_device(comm) != j.gpu)
+      fail(SLLM_E_INVALID, "communicator belongs to another GPU");
+    if (j.dst_base && (reinterpret_cast<uintptr_t>(j.dst_base) & 15)) fail(SLLM_E_INVALID, "dst_base must be 16-byte aligned");
+    if (scatter) {
+      for (uint32_t ti : idx->parts[p].by_offset) {
+        if (!dst_tensor[ti]) fail(SLLM_E_INVALID, "null destination for tensor '" + idx->tensors[ti].name + "'");
+        if (reinterpret_cast<uintptr_t>(dst_tensor[ti]) & 15)
+          fail(SLLM_E_INVALID, "destination of '" + idx->tensors[ti].name + "' is not 16-byte aligned");
+      }
+    }
+    // the source must be page-locked host memory ("pinned memory ... DMA")
+    cudaPointerAttributes at{};
+    SLLM_CUDA(cudaSetDevice(j.gpu));
+    if (cudaPointerGetAttributes(&at, j.src) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      fail(SLLM_E_INVALID, "partition source is not pinned host memory (use sllm_host_alloc / sllm_host_register)");
+    }
+    j.src_dev = static_cast<const uint8_t*>(at.devicePointer);
+    if ((cfg.mode == SLLM_MODE_ZEROCOPY || cfg.mode == SLLM_MODE_SCATTER_ZC) && !j.src_dev)
+      fail(SLLM_E_INVALID, "zero-copy modes need host memory mapped into the device address space");
+    build_segments(*idx, j, scatter, L->dst_tensor, cfg.chunk_bytes);
+    L->jobs.push_back(std::move(j));
+  }
+  // busy set
+  {
+    std::lock_guard<std::mutex> g(g_busy_mu);
+    std::vector<const void*> keys;
+    for (auto& j : L->jobs) {
+      if (j.dst_base) keys.push_back(j.dst_base);
+      if (scatter)
+        for (uint32_t ti : idx->parts[j.p].by_offset) keys.push_back(L->dst_tensor[ti]);
+    }
+    for (const void* k : keys)
+      if (g_busy.count(k)) fail(SLLM_E_BUSY, "destination is already being loaded");
+    for (const void* k : keys) g_busy.insert(k);
+    L->busy_keys = std::move(keys);
+  }
+  for (auto& j : L->jobs) j.th = std::thread(run_job_guarded, L.get(), std::ref(j));
+  return L.release();
+}
+
+static void join_load(sllm_load* L) {
+  if (L->joined) return;
+  for (auto& j : L->jobs)
+    if (j.th.joinable()) j.th.join();
+  L->joined = true;
+  {
+    std::lock_guard<std::mutex> g(g_busy_mu);
+    for (const void* k : L->busy_keys) g_busy.erase(k);
+    L->busy_keys.clear();
+  }
+  sllm_load_report& r = L->rep;
+  r = sllm_load_report{};
+  r.bad_partition = -1;
+  r.bad_block = ~0ull;
+  r.mode = L->cfg.mode;
+  sllm_status st = SLLM_OK;
+  std::string err;
+  for (auto& j : L->jobs) {
+    for (uint32_t ti : L->idx->parts[j.p].by_offset) r.payload_bytes += L->idx->tensors[ti].nbytes;
+    r.transferred_bytes += j.transferred;
+    r.fanout_bytes += j.fanout;
+    r.chunks += j.chunks;
+    r.kernel_launches += j.launches;
+    r.copy_calls += j.copies;
+    r.t_issue_ns_max = std::max(r.t_issue_ns_max, j.t_issue_ns);
+    r.t_device_ms_max = std::max(r.t_device_ms_max, (double)j.t_dev_ms);
+    r.t_kernel_ms_sum += j.kernel_ms;
+    r.t_copy_ms_sum += j.copy_ms;
+    r.kernel_bytes += j.kernel_bytes;
+    if (j.status != SLLM_OK && st == SLLM_OK) {
+      st = j.status;
+      err = j.error;
+    }
+    if (j.status == SLLM_OK && j.h_bad != ~0ull && r.bad_partition < 0) {
+      r.bad_partition = (int32_t)j.p;
+      r.bad_block = j.h_bad;
+    }
+  }
+  if (st == SLLM_OK && r.bad_partition >= 0) {
+    st = SLLM_E_CHECKSUM;
+    err = "checksum mismatch in partition " + std::to_string(r.bad_partition) + ", block " + std::to_string(r.bad_block);
+  }
+  r.t_total_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - L->t0).count();
+  L->result = st;
+  if (st != SLLM_OK) set_last_error(err);
+}
+
+sllm_status sllm_load_wait_internal(sllm_load* L, sllm_load_report* rep) {
+  join_load(L);
+  if (rep) *rep = L->rep;
+  if (L->result != SLLM_OK) {
+    for (auto& j : L->jobs)
+      if (j.status != SLLM_OK) { set_last_error(j.error); break; }
+    if (L->result == SLLM_E_CHECKSUM)
+      set_last_error("checksum mismatch in partition " + std::to_string(L->rep.bad_partition) + ", block " +
+                     std::to_string(L->rep.bad_block));
+  }
+  return L->result;
+}
+
+void sllm_load_tensor_internal(const sllm_load* L, const char* name, sllm_tensor_handle* h) {
+  if (!name || !h) fail(SLLM_E_INVALID, "null argument");
+  auto it = L->idx->by_name.find(name);
+  if (it == L->idx->by_name.end()) fail(SLLM_E_LOOKUP, std::string("unknown tensor '") + name + "'");
+  const TensorRec& t = L->idx->tensors[it->second];
+  const PartJob* job = nullptr;
+  for (auto& j : L->jobs)
+    if ((int32_t)j.p == t.part) job = &j;
+  if (!job) fail(SLLM_E_LOOKUP, "tensor '" + t.name + "' belongs to a partition this load does not handle");
+  sllm_tensor_handle o{};
+  o.gpu = job->gpu;
+  o.dtype = t.dtype;
+  o.ndim = t.ndim;
+  std::memcpy(o.shape, t.shape, sizeof o.shape);
+  o.ptr = L->dst_tensor.empty() ? (void*)(job->dst_base + t.offset) : L->dst_tensor[it->second];
+  o.nbytes = t.nbytes;
+  *h = o;
+}
+
+void sllm_load_block_checksums_internal(sllm_load* L, size_t p, const uint64_t** table) {
+  join_load(L);
+  for (auto& j : L->jobs) {
+    if (j.p != p) continue;
+    if (!j.h_cs_valid) {
+      j.h_cs.assign(L->idx->parts[p].n_blocks, 0);
+      if (!j.h_cs.empty() && j.d_cs) {
+        SLLM_CUDA(cudaSetDevice(j.gpu));
+        SLLM_CUDA(cudaMemcpy(j.h_cs.data(), j.d_cs, j.h_cs.size() * 8, cudaMemcpyDeviceToHost));
+      }
+      j.h_cs_valid = true;
+    }
+    *table = j.h_cs.data();
+    return;
+  }
+  fail(SLLM_E_LOOKUP, "partition not handled by this load");
+}
+
+void sllm_load_free_internal(sllm_load* L) {
+  join_load(L);
+  for (auto& j : L->jobs) {
+    if (j.gpu >= 0) cudaSetDevice(j.gpu);
+    if (j.scratch) cudaFreeAsync(j.scratch, device_ctx(j.gpu).streams[0]);
+    for (auto& e : j.ev)
+      if (e) cudaEventDestroy(e);
+  }
+  delete L;
+}

@@ -1,0 +1,47 @@
+// Host runtime internals: per-GPU contexts, NCCL shim, load objects.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <mutex>
+#include <thread>
+
+#include "common.hpp"
+#include "kernels.cuh"
+
+namespace sllm {
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what);
+#define SLLM_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) ::sllm::cuda_fail(_e, #call);  \
+  } while (0)
+
+constexpr int kMaxStreams = 8;
+constexpr uint32_t kTile = 64u << 10;  // bytes per kernel work tile
+
+// Library-owned, per-GPU resources reused across loads (no allocation in the hot path).
+struct DeviceCtx {
+  int dev = -1;
+  std::mutex mu;
+  cudaStream_t streams[kMaxStreams] = {};
+  cudaStream_t comm_stream = nullptr;
+  void* staging[kMaxStreams] = {};
+  uint64_t staging_bytes = 0;
+  void ensure(int n_streams);                          // caller holds mu, device set
+  void ensure_staging(int n, uint64_t bytes);          // caller holds mu, device set
+};
+DeviceCtx& device_ctx(int dev);
+
+// ---- NCCL (loaded with dlopen; only the calls the fan-out needs) -------------------
+struct Nccl;
+const Nccl& nccl();  // throws SLLM_E_NCCL if libnccl.so.2 cannot be loaded
+void nccl_bcast_group(sllm_comm* comm, const std::vector<std::pair<uint64_t, uint64_t>>& ranges_by_root,
+                      uint8_t* buf, cudaStream_t s);
+int comm_nranks(const sllm_comm* c);
+int comm_rank(const sllm_comm* c);
+int comm_device(const sllm_comm* c);
+
+}  // namespace sllm

@@ -18,3 +18,12 @@ def csynth():
     from synth import payload
     payload.build_csynth()
     return payload
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_libraries():
+    """Build libsynth.so (input generator) and libsllm.so (the product) in-tree."""
+    from synth import payload
+    payload.build_csynth()
+    from paper_2401_14351_b200 import build
+    build.build()
