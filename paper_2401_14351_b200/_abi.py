@@ -40,7 +40,8 @@ class TensorInfo(C.Structure):
 
 class LoadConfig(C.Structure):
     _fields_ = [("chunk_bytes", C.c_uint64), ("n_streams", C.c_int32), ("mode", C.c_int32), ("fanout", C.c_int32),
-                ("verify", C.c_int32), ("ctas", C.c_int32), ("profile", C.c_int32)]
+                ("verify", C.c_int32), ("ctas", C.c_int32), ("profile", C.c_int32),
+                ("engine", C.c_int32), ("reserved", C.c_int32)]
 
 
 class LoadReport(C.Structure):

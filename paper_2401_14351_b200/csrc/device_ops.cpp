@@ -43,6 +43,7 @@ void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint6
   mp.acc = reinterpret_cast<BlockAcc*>(b);
   mp.cs_out = out;
   mp.bad = bad;
+  mp.engine = 1;
   SLLM_CUDA(launch_materialise(mp, MatKind::kChecksumOnly, ctas > 0 ? ctas : default_grid(), st));
   SLLM_CUDA(cudaFreeAsync(scratch, st));
 }
@@ -93,6 +94,7 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   mp.acc = d_acc;
   mp.expect = check ? d_expect : nullptr;
   mp.bad = d_bad;
+  mp.engine = 1;
   SLLM_CUDA(launch_materialise(mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas > 0 ? ctas : default_grid(), st));
   unsigned long long bad = ~0ull;
   SLLM_CUDA(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st));

@@ -165,11 +165,212 @@ __global__ void __launch_bounds__(kThreads) materialise_kernel(const MatParams p
   }
 }
 
+
+// ---------------------------------------------------------------------------------
+// TMA-staged variant (default engine).  One CTA = 1 producer warp + 8 consumer warps.
+// The producer streams the CTA's blocks through a 12-stage shared-memory ring with
+// 1-D bulk copies (cp.async.bulk, completion counted on an mbarrier); the consumers
+// read each 16 KiB stage with 16-byte LDS, store the tensor bytes to their destination
+// and accumulate the closed-form checksum terms.  A CTA owns whole checksum blocks, so
+// a block is reduced once inside the CTA -- no global atomics, no fences.  192 KiB in
+// flight per SM covers HBM latency (K3/K4) and, with a few CTAs, PCIe latency (K2).
+// ---------------------------------------------------------------------------------
+constexpr int kConsumerWarps = 8;
+constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
+constexpr uint32_t kStageBytes = 16u << 10;
+constexpr int kStages = 12;
+constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + 2 * kStages * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+// Parity wait with a watchdog: a transfer that never completes (e.g. an unmapped source)
+// traps after ~20 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(smem_addr(b)), "r"(parity) : "memory");
+    if (done) return;
+    if ((it & 1023) == 1023) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (!t0) t0 = t;
+      else if (t - t0 > 20000000000ull) __trap();
+    }
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ uint4 lds16(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(smem_addr(p)));
+  return r;
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory"); }
+
+template <bool kStore, bool kCheck>
+__global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const MatParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  __shared__ unsigned long long s_red[3][kConsumerWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t unit = kCheck ? p.block : (1ull << 20);  // a CTA owns whole units
+  const uint64_t u_first = p.lo / unit, u_end = (p.hi + unit - 1) / unit;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // producer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x) {
+        const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
+        for (uint64_t off = a; off < e; off += kStageBytes) {
+          const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], n);
+          bulk_g2s(smem + (size_t)stage * kStageBytes, p.src + (off - p.src_origin), n, &full[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  const int ct = threadIdx.x - 32;  // consumer thread 0..255
+  const int cw = warp - 1;
+  uint32_t stage = 0, phase = 0;
+  for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x) {
+    const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
+    // segment holding byte a (same search in every thread: uniform, L1-cached)
+    uint32_t cur = p.seg_begin;
+    if (kStore) {
+      uint32_t lo = p.seg_begin, hi = p.seg_end;
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (p.segs[mid].off <= a) lo = mid; else hi = mid;
+      }
+      cur = lo;
+    }
+    Seg sg = kStore ? p.segs[cur] : Seg{0, 0, nullptr, 0};
+    unsigned long long A = 0, Bs = 0, Cs = 0;
+    for (uint64_t off = a; off < e; off += kStageBytes) {
+      const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
+      mbar_wait(&full[stage], phase);
+      const uint8_t* sb = smem + (size_t)stage * kStageBytes;
+#pragma unroll 4
+      for (uint32_t v = (uint32_t)ct * 16; v < n; v += 32 * kConsumerWarps * 16) {
+        const uint4 val = lds16(sb + v);
+        const uint64_t x = off + v;
+        if (kStore) {
+          while (x >= sg.off + sg.len && cur + 1 < p.seg_end) sg = p.segs[++cur];
+          if (sg.dst) {
+            const uint64_t rel = x - sg.off;
+            if (rel + 16 <= sg.valid) store16(sg.dst + rel, val);
+            else if (rel < sg.valid) store_partial(sg.dst + rel, val, (uint32_t)(sg.valid - rel));
+          }
+        }
+        if (kCheck) {
+          const uint32_t i0 = (uint32_t)((x - u * unit) >> 2);
+          const unsigned long long s4 = (unsigned long long)val.x + val.y + val.z + val.w;
+          A += s4;
+          Bs += (unsigned long long)i0 * s4;
+          Cs += (unsigned long long)val.y + 2ull * val.z + 3ull * val.w;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kStages) { stage = 0; phase ^= 1; }
+      if (kCheck) {
+        A = fold(A);
+        Bs = fold(Bs);
+        Cs = fold(Cs);
+      }
+    }
+    if (kCheck) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        A += __shfl_xor_sync(0xffffffffu, A, o);
+        Bs += __shfl_xor_sync(0xffffffffu, Bs, o);
+        Cs += __shfl_xor_sync(0xffffffffu, Cs, o);
+      }
+      if (lane == 0) {
+        s_red[0][cw] = A;
+        s_red[1][cw] = Bs;
+        s_red[2][cw] = Cs;
+      }
+      consumer_sync();
+      if (ct == 0) {
+        unsigned long long SA = 0, SB = 0, SC = 0;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) {
+          SA += s_red[0][w];
+          SB += s_red[1][w];
+          SC += s_red[2][w];
+        }
+        const unsigned long long fa = fold(SA), fb = fold(SB), fc = fold(SC);
+        const unsigned long long nw = ((e - u * unit) >> 2) % kM;
+        const unsigned long long s2 = fold(fold(nw * fa) + (kM - fb) + (kM - fc));
+        const unsigned long long cs = (s2 << 32) | fa;
+        if (p.cs_out) p.cs_out[u] = cs;
+        if (p.expect && p.expect[u] != cs) atomicMin(p.bad, (unsigned long long)u);
+      }
+      consumer_sync();
+    }
+  }
+}
+
 }  // namespace
+
+template <bool kStore, bool kCheck>
+static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream) {
+  static bool configured = false;  // per template instance
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(materialise_tma_kernel<kStore, kCheck>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const uint64_t unit = kCheck ? p.block : (1ull << 20);
+  const uint64_t units = (p.hi + unit - 1) / unit - p.lo / unit;
+  if ((uint64_t)grid > units) grid = (int)units;
+  materialise_tma_kernel<kStore, kCheck><<<grid, kTmaThreads, kTmaSmem, stream>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream) {
   if (p.hi <= p.lo) return cudaSuccess;
   if (grid < 1) grid = 1;
+  if (p.engine == 1) {
+    switch (kind) {
+      case MatKind::kChecksumOnly: return launch_tma<false, true>(p, grid, stream);
+      case MatKind::kCopyChecksum: return launch_tma<true, true>(p, grid, stream);
+      case MatKind::kCopyOnly: return launch_tma<true, false>(p, grid, stream);
+    }
+  }
   const uint64_t ntiles = (p.hi - p.lo + p.tile - 1) / p.tile;
   if ((uint64_t)grid > ntiles) grid = (int)ntiles;
   switch (kind) {

@@ -40,6 +40,7 @@ struct MatParams {
   uint64_t* cs_out;          // computed block checksums, or nullptr
   unsigned long long* bad;   // min failing block index (init UINT64_MAX)
   int host_src;              // 1: src is host-mapped pinned memory (zero-copy over PCIe)
+  int engine;                // 0: LDG/STG tiles; 1: TMA bulk copies through a shared-memory ring
 };
 
 enum class MatKind : int {

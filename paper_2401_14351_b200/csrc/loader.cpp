@@ -41,19 +41,17 @@ DeviceCtx& device_ctx(int dev) {
 }
 
 void DeviceCtx::ensure(int n) {
+  if (!streams[0]) {  // keep stream-ordered allocations (scratch, staging) cached between loads
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   for (int s = 0; s < n; ++s)
     if (!streams[s]) SLLM_CUDA(cudaStreamCreateWithFlags(&streams[s], cudaStreamNonBlocking));
   if (!comm_stream) SLLM_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
-}
-
-void DeviceCtx::ensure_staging(int n, uint64_t bytes) {
-  if (bytes > staging_bytes) {
-    for (auto& p : staging)
-      if (p) { SLLM_CUDA(cudaFree(p)); p = nullptr; }
-    staging_bytes = bytes;
-  }
-  for (int s = 0; s < n; ++s)
-    if (!staging[s]) SLLM_CUDA(cudaMalloc(&staging[s], staging_bytes));
 }
 
 // ------------------------------------------------------------------------------------
@@ -78,6 +76,7 @@ struct PartJob {
   std::vector<uint32_t> chunk_seg;  // first segment of each chunk of [0, L)
   // device scratch (one cudaMallocAsync block)
   void* scratch = nullptr;
+  uint8_t* staging = nullptr;  // SCATTER_CE ring: n_streams slots of chunk_bytes (per job)
   Seg* d_segs = nullptr;
   BlockAcc* d_acc = nullptr;
   uint64_t* d_expect = nullptr;
@@ -218,6 +217,7 @@ static void issue_chunk(const sllm_index& idx, const sllm_load_config& cfg, Devi
   mp.expect = check ? j.d_expect : nullptr;
   mp.cs_out = check ? j.d_cs : nullptr;
   mp.bad = j.d_bad;
+  mp.engine = cfg.engine == 2 ? 0 : 1;
   switch (cfg.mode) {
     case SLLM_MODE_CE:
       copy_h2d(j, prof, j.dst_base + lo, j.src + lo, hi - lo, st);
@@ -236,8 +236,8 @@ static void issue_chunk(const sllm_index& idx, const sllm_load_config& cfg, Devi
       launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, st);
       break;
     case SLLM_MODE_SCATTER_CE:
-      copy_h2d(j, prof, dc.staging[slot], j.src + lo, hi - lo, st);
-      mp.src = static_cast<const uint8_t*>(dc.staging[slot]);
+      copy_h2d(j, prof, j.staging + (uint64_t)slot * cfg.chunk_bytes, j.src + lo, hi - lo, st);
+      mp.src = j.staging + (uint64_t)slot * cfg.chunk_bytes;
       mp.src_origin = lo;
       mp.host_src = 0;
       launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, st);
@@ -266,6 +266,7 @@ static void verify_range(const sllm_index& idx, const sllm_load_config& cfg, Par
   mp.expect = j.d_expect;
   mp.cs_out = j.d_cs;
   mp.bad = j.d_bad;
+  mp.engine = cfg.engine == 2 ? 0 : 1;
   launch(j, cfg.profile != 0, mp, MatKind::kChecksumOnly, cfg.ctas > 0 ? cfg.ctas : 64, st);
 }
 
@@ -279,7 +280,6 @@ static void run_job(sllm_load* L, PartJob& j) {
   {
     std::lock_guard<std::mutex> g(dc.mu);
     dc.ensure(cfg.n_streams);
-    if (cfg.mode == SLLM_MODE_SCATTER_CE) dc.ensure_staging(cfg.n_streams, cfg.chunk_bytes);
   }
   cudaStream_t s0 = dc.streams[0];
   for (auto& e : j.ev) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
@@ -293,6 +293,11 @@ static void run_job(sllm_load* L, PartJob& j) {
     SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[3], 0));
   }
   SLLM_CUDA(cudaMallocAsync(&j.scratch, total, s0));
+  if (cfg.mode == SLLM_MODE_SCATTER_CE) {
+    void* st = nullptr;
+    SLLM_CUDA(cudaMallocAsync(&st, (size_t)cfg.n_streams * cfg.chunk_bytes, s0));
+    j.staging = static_cast<uint8_t*>(st);
+  }
   uint8_t* base = static_cast<uint8_t*>(j.scratch);
   j.d_segs = reinterpret_cast<Seg*>(base);
   j.d_acc = reinterpret_cast<BlockAcc*>(base + seg_bytes);
@@ -411,6 +416,8 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (cfg.n_streams < 1 || cfg.n_streams > kMaxStreams) fail(SLLM_E_INVALID, "n_streams must be in 1..8");
   if (cfg.mode < SLLM_MODE_CE || cfg.mode > SLLM_MODE_SCATTER_ZC) fail(SLLM_E_INVALID, "unknown mode");
   if (cfg.profile != 0 && cfg.profile != 1) fail(SLLM_E_INVALID, "profile must be 0 or 1");
+  if (cfg.engine < 0 || cfg.engine > 2) fail(SLLM_E_INVALID, "unknown kernel engine");
+  if (cfg.reserved) fail(SLLM_E_INVALID, "reserved config field must be 0");
   if (cfg.chunk_bytes % tile_for(*idx)) fail(SLLM_E_INVALID, "chunk size must be a multiple of the 64 KiB work tile");
   if (idx->block && cfg.chunk_bytes % idx->block) fail(SLLM_E_INVALID, "chunk size must be a multiple of the block size");
   if (cfg.chunk_bytes % idx->align) fail(SLLM_E_INVALID, "chunk size must be a multiple of the alignment");
@@ -584,6 +591,7 @@ void sllm_load_free_internal(sllm_load* L) {
   for (auto& j : L->jobs) {
     if (j.gpu >= 0) cudaSetDevice(j.gpu);
     if (j.scratch) cudaFreeAsync(j.scratch, device_ctx(j.gpu).streams[0]);
+    if (j.staging) cudaFreeAsync(j.staging, device_ctx(j.gpu).streams[0]);
     for (auto& e : j.ev)
       if (e) cudaEventDestroy(e);
   }

@@ -28,10 +28,7 @@ struct DeviceCtx {
   std::mutex mu;
   cudaStream_t streams[kMaxStreams] = {};
   cudaStream_t comm_stream = nullptr;
-  void* staging[kMaxStreams] = {};
-  uint64_t staging_bytes = 0;
   void ensure(int n_streams);                          // caller holds mu, device set
-  void ensure_staging(int n, uint64_t bytes);          // caller holds mu, device set
 };
 DeviceCtx& device_ctx(int dev);
 

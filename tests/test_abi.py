@@ -79,19 +79,19 @@ def test_load_rejects_bad_arguments():
     idx.seal([buf.ctypes.data])
     lib = sllm.lib()
     out = ctypes.c_void_p()
-    cfg = _abi.LoadConfig(3 << 20 | 5, 2, 0, 0, 1, 0, 0)   # chunk not a multiple of the block
+    cfg = _abi.LoadConfig(3 << 20 | 5, 2, 0, 0, 1, 0, 0, 0, 0)   # chunk not a multiple of the block
     gpu = (ctypes.c_int32 * 1)(0)
     src = (ctypes.c_void_p * 1)(buf.ctypes.data)
     dst = (ctypes.c_void_p * 1)(0x1000)
     st = lib.sllm_load_start(idx.handle, ctypes.byref(cfg), src, gpu, dst, None, None, None, ctypes.byref(out))
     assert st == _abi.E_INVALID
-    cfg = _abi.LoadConfig(1 << 20, 9, 0, 0, 1, 0, 0)        # too many streams
+    cfg = _abi.LoadConfig(1 << 20, 9, 0, 0, 1, 0, 0, 0, 0)        # too many streams
     st = lib.sllm_load_start(idx.handle, ctypes.byref(cfg), src, gpu, dst, None, None, None, ctypes.byref(out))
     assert st == _abi.E_INVALID
-    cfg = _abi.LoadConfig(1 << 20, 2, 7, 0, 1, 0, 0)        # unknown mode
+    cfg = _abi.LoadConfig(1 << 20, 2, 7, 0, 1, 0, 0, 0, 0)        # unknown mode
     st = lib.sllm_load_start(idx.handle, ctypes.byref(cfg), src, gpu, dst, None, None, None, ctypes.byref(out))
     assert st == _abi.E_INVALID
     unsealed = sllm.Index.plan([("a", 0, "u8", (10,))], 4096, 4096)
-    cfg = _abi.LoadConfig(1 << 20, 2, 0, 0, 1, 0, 0)
+    cfg = _abi.LoadConfig(1 << 20, 2, 0, 0, 1, 0, 0, 0, 0)
     st = lib.sllm_load_start(unsealed.handle, ctypes.byref(cfg), src, gpu, dst, None, None, None, ctypes.byref(out))
     assert st == _abi.E_INVALID

@@ -49,13 +49,14 @@ def check_against_oracle(res, idx, inv, lay, oparts, payloads, parts_loaded, cfg
             assert res.block_checksums(p).tolist() == lay.checksums[d]
 
 
+@pytest.mark.parametrize("engine", ["tma", "ldg"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("chunk,streams", [(1 << 20, 1), (2 << 20, 2), (4 << 20, 3), (16 << 20, 2)])
-def test_toy_all_modes(mode, chunk, streams):
+def test_toy_all_modes(mode, chunk, streams, engine):
     inv, seed = models.model_inventory("toy")
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
     lay, oparts, payloads = oracle_of(inv, seed, 4096, 1 << 20)
-    cfg = sllm.LoadConfig(chunk_bytes=chunk, n_streams=streams, mode=mode)
+    cfg = sllm.LoadConfig(chunk_bytes=chunk, n_streams=streams, mode=mode, engine=engine)
     res = sllm.load(idx, bufs, {0: 0}, cfg)
     rep = res.report
     assert rep["bad_partition"] == -1 and rep["payload_bytes"] == 13_569_860
@@ -64,13 +65,14 @@ def test_toy_all_modes(mode, chunk, streams):
     check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
 
 
+@pytest.mark.parametrize("engine", ["tma", "ldg"])
 @pytest.mark.parametrize("mode", MODES)
-def test_toy_align16_and_small_blocks(mode):
+def test_toy_align16_and_small_blocks(mode, engine):
     inv, seed = models.model_inventory("toy")
     for A, B, C in [(16, 1 << 20, 1 << 20), (16, 4096, 1 << 20), (256, 1 << 16, 3 << 16)]:
         idx, bufs = workloads.build_pinned(inv, seed, A, B)
         lay, oparts, payloads = oracle_of(inv, seed, A, B)
-        cfg = sllm.LoadConfig(chunk_bytes=C, n_streams=2, mode=mode, ctas=7)
+        cfg = sllm.LoadConfig(chunk_bytes=C, n_streams=2, mode=mode, ctas=7, engine=engine)
         res = sllm.load(idx, bufs, {0: 0}, cfg)
         check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
 
@@ -88,14 +90,15 @@ def test_random_checkpoints(seed):
     mode = MODES[seed % 4]
     chunk = B * int(rng.integers(1, 5)) if B >= 1 << 16 else 1 << 16
     cfg = sllm.LoadConfig(chunk_bytes=chunk, n_streams=int(rng.integers(1, 5)), mode=mode,
-                          ctas=int(rng.choice([0, 1, 5, 64])))
+                          ctas=int(rng.choice([0, 1, 5, 64])), engine=["tma", "ldg"][(seed // 4) % 2])
     n = len(idx.partitions)
     res = sllm.load(idx, bufs, {p: 0 for p in range(n)}, cfg)
     check_against_oracle(res, idx, inv, lay, oparts, payloads, list(range(n)), cfg)
 
 
+@pytest.mark.parametrize("engine", ["tma", "ldg"])
 @pytest.mark.parametrize("mode", MODES)
-def test_fault_injection_names_block(mode):
+def test_fault_injection_names_block(mode, engine):
     """A flipped source byte in block j yields SLLM_E_CHECKSUM(0, j) -- the same
     (partition, block) the oracle loader reports (O9(d))."""
     inv, seed = models.model_inventory("toy")
@@ -109,7 +112,7 @@ def test_fault_injection_names_block(mode):
         with pytest.raises(Exception) as oex:
             oloader.load(idx.serialize(), {0: host})
         assert (oex.value.partition, oex.value.block) == (0, pos // (1 << 20))
-        cfg = sllm.LoadConfig(chunk_bytes=2 << 20, mode=mode)
+        cfg = sllm.LoadConfig(chunk_bytes=2 << 20, mode=mode, engine=engine)
         bases, per_tensor = sllm.allocate(idx, {0: 0}, cfg.scatter)
         res = sllm.load_start(idx, bufs, {0: 0}, cfg, bases, per_tensor)
         with pytest.raises(sllm.SllmError) as ex:
