@@ -52,6 +52,7 @@ void DeviceCtx::ensure(int n) {
   for (int s = 0; s < n; ++s)
     if (!streams[s]) SLLM_CUDA(cudaStreamCreateWithFlags(&streams[s], cudaStreamNonBlocking));
   if (!comm_stream) SLLM_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+  if (!kern_stream) SLLM_CUDA(cudaStreamCreateWithFlags(&kern_stream, cudaStreamNonBlocking));
 }
 
 // ------------------------------------------------------------------------------------
@@ -195,37 +196,61 @@ static void copy_h2d(PartJob& j, bool prof, void* dst, const void* src, uint64_t
   j.copies++;
 }
 
-// Issue one chunk [lo, hi) of job j on stream st (slot = staging slot for SCATTER_CE).
-static void issue_chunk(const sllm_index& idx, const sllm_load_config& cfg, DeviceCtx& dc, PartJob& j,
-                        uint64_t k, uint64_t lo, uint64_t hi, int slot, cudaStream_t st) {
-  const PartRec& pr = idx.parts[j.p];
+// Streams of one job: S transfer streams (copy engine or zero-copy kernels) and one
+// kernel stream for the verify / scatter kernels that follow a copy-engine transfer, so
+// the copy engine always has the next chunk queued (no per-chunk kernel in its way).
+struct Pipe {
+  cudaStream_t xfer[kMaxStreams] = {};
+  int S = 1;
+  cudaStream_t kern = nullptr;
+  cudaEvent_t copied = nullptr;            // chunk k landed (recorded, then waited at once)
+  std::vector<cudaEvent_t> freed;          // SCATTER_CE: staging slot reusable
+  int nslot = 0;
+};
+
+static MatParams chunk_params(const sllm_index& idx, const sllm_load_config& cfg, const PartJob& j, uint64_t k,
+                              uint64_t lo, uint64_t hi) {
   const bool check = cfg.verify && idx.block;
-  const bool prof = cfg.profile != 0;
-  const int ctas = cfg.ctas > 0 ? cfg.ctas : default_ctas(cfg.mode);
   MatParams mp{};
   mp.lo = lo;
   mp.hi = hi;
   mp.segs = j.d_segs;
   mp.seg_begin = j.chunk_seg[k];
-  uint64_t nch = j.chunk_seg.size() - 1;
+  const uint64_t nch = j.chunk_seg.size() - 1;
   mp.seg_end = k + 1 < nch ? std::min<uint32_t>(j.chunk_seg[k + 1] + 1, (uint32_t)j.segs.size())
                            : (uint32_t)j.segs.size();
   mp.tile = tile_for(idx);
   mp.block = idx.block ? idx.block : kTile;
-  mp.part_len = pr.length;
+  mp.part_len = idx.parts[j.p].length;
   mp.acc = j.d_acc;
   mp.expect = check ? j.d_expect : nullptr;
   mp.cs_out = check ? j.d_cs : nullptr;
   mp.bad = j.d_bad;
   mp.engine = cfg.engine == 2 ? 0 : 1;
+  return mp;
+}
+
+// Issue chunk k = [lo, hi) of job j.  Returns the stream whose completion means "chunk k
+// is in place and verified" (used by the fan-out to order the broadcast after it).
+static cudaStream_t issue_chunk(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, Pipe& P, uint64_t k,
+                                uint64_t lo, uint64_t hi) {
+  const bool check = cfg.verify && idx.block;
+  const bool prof = cfg.profile != 0;
+  const int ctas = cfg.ctas > 0 ? cfg.ctas : default_ctas(cfg.mode);
+  MatParams mp = chunk_params(idx, cfg, j, k, lo, hi);
+  cudaStream_t xs = P.xfer[k % P.S];
+  cudaStream_t done = xs;
   switch (cfg.mode) {
     case SLLM_MODE_CE:
-      copy_h2d(j, prof, j.dst_base + lo, j.src + lo, hi - lo, st);
+      copy_h2d(j, prof, j.dst_base + lo, j.src + lo, hi - lo, xs);
       if (check) {
+        SLLM_CUDA(cudaEventRecord(P.copied, xs));
+        SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
         mp.src = j.dst_base;
         mp.src_origin = 0;
         mp.host_src = 0;
-        launch(j, prof, mp, MatKind::kChecksumOnly, ctas, st);
+        launch(j, prof, mp, MatKind::kChecksumOnly, ctas, P.kern);
+        done = P.kern;
       }
       break;
     case SLLM_MODE_ZEROCOPY:
@@ -233,20 +258,29 @@ static void issue_chunk(const sllm_index& idx, const sllm_load_config& cfg, Devi
       mp.src = j.src_dev;
       mp.src_origin = 0;
       mp.host_src = 1;
-      launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, st);
+      launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, xs);
       break;
-    case SLLM_MODE_SCATTER_CE:
-      copy_h2d(j, prof, j.staging + (uint64_t)slot * cfg.chunk_bytes, j.src + lo, hi - lo, st);
-      mp.src = j.staging + (uint64_t)slot * cfg.chunk_bytes;
+    case SLLM_MODE_SCATTER_CE: {
+      const int slot = (int)(k % (uint64_t)P.nslot);
+      uint8_t* stage = j.staging + (uint64_t)slot * cfg.chunk_bytes;
+      if (k >= (uint64_t)P.nslot) SLLM_CUDA(cudaStreamWaitEvent(xs, P.freed[slot], 0));
+      copy_h2d(j, prof, stage, j.src + lo, hi - lo, xs);
+      SLLM_CUDA(cudaEventRecord(P.copied, xs));
+      SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
+      mp.src = stage;
       mp.src_origin = lo;
       mp.host_src = 0;
-      launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, st);
+      launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, P.kern);
+      SLLM_CUDA(cudaEventRecord(P.freed[slot], P.kern));
+      done = P.kern;
       break;
+    }
     default:
       fail(SLLM_E_INVALID, "unknown mode");
   }
   j.chunks++;
   j.transferred += hi - lo;
+  return done;
 }
 
 // Checksum-only verification of bytes that arrived through the fan-out.
@@ -281,7 +315,17 @@ static void run_job(sllm_load* L, PartJob& j) {
     std::lock_guard<std::mutex> g(dc.mu);
     dc.ensure(cfg.n_streams);
   }
-  cudaStream_t s0 = dc.streams[0];
+  Pipe P;
+  P.S = cfg.n_streams;
+  for (int s = 0; s < P.S; ++s) P.xfer[s] = dc.streams[s];
+  P.kern = dc.kern_stream;
+  P.nslot = std::max(3, P.S + 1);
+  SLLM_CUDA(cudaEventCreateWithFlags(&P.copied, cudaEventDisableTiming));
+  if (cfg.mode == SLLM_MODE_SCATTER_CE) {
+    P.freed.resize(P.nslot);
+    for (auto& e : P.freed) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t s0 = P.xfer[0];
   for (auto& e : j.ev) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
   const uint64_t nb = pr.n_blocks;
   const size_t seg_bytes = align_up(j.segs.size() * sizeof(Seg), 256);
@@ -295,7 +339,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   SLLM_CUDA(cudaMallocAsync(&j.scratch, total, s0));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
     void* st = nullptr;
-    SLLM_CUDA(cudaMallocAsync(&st, (size_t)cfg.n_streams * cfg.chunk_bytes, s0));
+    SLLM_CUDA(cudaMallocAsync(&st, (size_t)P.nslot * cfg.chunk_bytes, s0));
     j.staging = static_cast<uint8_t*>(st);
   }
   uint8_t* base = static_cast<uint8_t*>(j.scratch);
@@ -305,16 +349,19 @@ static void run_job(sllm_load* L, PartJob& j) {
   j.d_cs = reinterpret_cast<uint64_t*>(base + seg_bytes + acc_bytes + tab_bytes);
   j.d_bad = reinterpret_cast<unsigned long long*>(base + seg_bytes + acc_bytes + 2 * tab_bytes);
   SLLM_CUDA(cudaMemcpyAsync(j.d_segs, j.segs.data(), j.segs.size() * sizeof(Seg), cudaMemcpyHostToDevice, s0));
-  SLLM_CUDA(cudaMemsetAsync(j.d_acc, 0, acc_bytes + tab_bytes, s0));  // accumulators (+ expect, overwritten)
+  SLLM_CUDA(cudaMemsetAsync(j.d_acc, 0, acc_bytes, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_cs, 0, tab_bytes, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_bad, 0xFF, 8, s0));
   if (nb) SLLM_CUDA(cudaMemcpyAsync(j.d_expect, pr.checksums.data(), nb * 8, cudaMemcpyHostToDevice, s0));
   SLLM_CUDA(cudaEventRecord(j.ev[0], s0));
   SLLM_CUDA(cudaEventRecord(j.ev[2], s0));
-  const int S = cfg.n_streams;
-  for (int s = 1; s < S; ++s) SLLM_CUDA(cudaStreamWaitEvent(dc.streams[s], j.ev[2], 0));
+  for (int s = 1; s < P.S; ++s) SLLM_CUDA(cudaStreamWaitEvent(P.xfer[s], j.ev[2], 0));
+  SLLM_CUDA(cudaStreamWaitEvent(P.kern, j.ev[2], 0));
 
   const uint64_t C = cfg.chunk_bytes;
+  std::vector<cudaStream_t> tails;  // streams to join at the end
+  for (int s = 1; s < P.S; ++s) tails.push_back(P.xfer[s]);
+  tails.push_back(P.kern);
   if (cfg.fanout == SLLM_FANOUT_BCAST) {
     // Replicated load: this rank moves its slice over PCIe; every chunk
     // round is then broadcast from its owner over NVLink (grouped, one root per slice).
@@ -323,18 +370,17 @@ static void run_job(sllm_load* L, PartJob& j) {
     if (sllm_replica_slices(pr.length, C, R, lohi.data()) != SLLM_OK) fail(SLLM_E_INVALID, "slice plan failed");
     uint64_t rounds = 0;
     for (int q = 0; q < R; ++q) rounds = std::max(rounds, ceil_div(lohi[2 * q + 1] - lohi[2 * q], C));
-    std::vector<cudaEvent_t> evk(rounds);
-    for (auto& e : evk) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t evk;
+    SLLM_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
     cudaStream_t cs = dc.comm_stream;
     SLLM_CUDA(cudaStreamWaitEvent(cs, j.ev[2], 0));
     for (uint64_t r = 0; r < rounds; ++r) {
       uint64_t lo = lohi[2 * me] + r * C;
       if (lo < lohi[2 * me + 1]) {
         uint64_t hi = std::min(lo + C, lohi[2 * me + 1]);
-        cudaStream_t st = dc.streams[r % S];
-        issue_chunk(idx, cfg, dc, j, lo / C, lo, hi, (int)(r % S), st);
-        SLLM_CUDA(cudaEventRecord(evk[r], st));
-        SLLM_CUDA(cudaStreamWaitEvent(cs, evk[r], 0));
+        cudaStream_t done = issue_chunk(idx, cfg, j, P, lo / C, lo, hi);
+        SLLM_CUDA(cudaEventRecord(evk, done));
+        SLLM_CUDA(cudaStreamWaitEvent(cs, evk, 0));
       }
       std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
       for (int q = 0; q < R; ++q) {
@@ -348,21 +394,17 @@ static void run_job(sllm_load* L, PartJob& j) {
         for (int q = 0; q < R; ++q)
           if (q != me && ranges[q].second > ranges[q].first) verify_range(idx, cfg, j, ranges[q].first, ranges[q].second, cs);
     }
-    SLLM_CUDA(cudaEventRecord(j.ev[2], cs));
-    SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[2], 0));
-    for (auto& e : evk) cudaEventDestroy(e);
+    tails.push_back(cs);
+    SLLM_CUDA(cudaEventDestroy(evk));
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
-    for (uint64_t k = 0; k < nch; ++k) {
-      uint64_t lo = k * C, hi = std::min(lo + C, pr.length);
-      issue_chunk(idx, cfg, dc, j, k, lo, hi, (int)(k % S), dc.streams[k % S]);
-    }
+    for (uint64_t k = 0; k < nch; ++k) issue_chunk(idx, cfg, j, P, k, k * C, std::min((k + 1) * C, pr.length));
   }
-  // join the streams into s0, then let the caller's stream wait for the load
-  for (int s = 1; s < S; ++s) {
+  // join every stream into s0, then let the caller's stream wait for the load
+  for (cudaStream_t t : tails) {
     cudaEvent_t e;
     SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    SLLM_CUDA(cudaEventRecord(e, dc.streams[s]));
+    SLLM_CUDA(cudaEventRecord(e, t));
     SLLM_CUDA(cudaStreamWaitEvent(s0, e, 0));
     SLLM_CUDA(cudaEventDestroy(e));  // destruction is deferred until the event completes
   }
@@ -384,6 +426,8 @@ static void run_job(sllm_load* L, PartJob& j) {
     (v == &j.kev ? j.kernel_ms : j.copy_ms) = sum;
     v->clear();
   }
+  cudaEventDestroy(P.copied);
+  for (auto& e : P.freed) cudaEventDestroy(e);
   SLLM_CUDA(cudaGetLastError());
 }
 

@@ -28,6 +28,7 @@ struct DeviceCtx {
   std::mutex mu;
   cudaStream_t streams[kMaxStreams] = {};
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t kern_stream = nullptr;
   void ensure(int n_streams);                          // caller holds mu, device set
 };
 DeviceCtx& device_ctx(int dev);
