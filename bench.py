@@ -41,8 +41,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="opt-6.7b")
-    ap.add_argument("--mode", default="zerocopy", choices=["ce", "zerocopy", "scatter_ce", "scatter_zc"])
-    ap.add_argument("--chunk-mib", type=int, default=16)
+    ap.add_argument("--mode", default="ce", choices=["ce", "zerocopy", "scatter_ce", "scatter_zc"])
+    ap.add_argument("--chunk-mib", type=int, default=64)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--cpu-sample-gib", type=float, default=4.0)
@@ -164,23 +164,29 @@ def cpu_baseline(args, bufs, idx, inv, seed):
                       f"copy every tensor, recompute+compare 1 MiB Fletcher-64 blocks; {dt:.1f} s"}
 
 
-def h2d_peak(bufs, bases, torch, gib=4, reps=5):
-    """B_h2d(1): cudaMemcpyAsync from the same pinned buffer into the same destination,
-    >= 4 GiB, best of `reps`."""
+def h2d_peak(bufs, bases, torch, gib=4, reps=3):
+    """B_h2d(1): the copy engine's best host->device rate from the same pinned buffer into
+    the same destination over >= 4 GiB: max of one 4 GiB
+    cudaMemcpyAsync and back-to-back 64 MiB cudaMemcpyAsync calls on one stream, best of
+    `reps` each.  Returns (GB/s, {method: GB/s})."""
     p = sorted(bufs)[0]
     n = min(gib << 30, bufs[p].nbytes)
     src = bufs[p].torch()[:n]
     dst = bases[p][:n]
-    best = 0.0
-    for _ in range(reps):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        s.record()
-        dst.copy_(src, non_blocking=True)
-        e.record()
-        e.synchronize()
-        best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)
-    return best
+    out = {}
+    for name, piece in (("single_4GiB", n), ("chunked_64MiB", 64 << 20)):
+        best = 0.0
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s.record()
+            for o in range(0, n, piece):
+                dst[o:o + piece].copy_(src[o:o + piece], non_blocking=True)
+            e.record()
+            e.synchronize()
+            best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)
+        out[name] = best
+    return max(out.values()), out
 
 
 def standalone_hbm(idx, torch, sllm, reps=5):
@@ -272,7 +278,7 @@ def main():
     payload_bytes = sum(t.nbytes for t in idx.tensors if t.partition in bufs)
     raw_bytes = sum(idx.partitions[p].length for p in parts)
 
-    b_h2d = h2d_peak(bufs, bases if not cfg.scatter else {p: torch.empty(min(4 << 30, idx.partitions[p].length),
+    b_h2d, b_h2d_methods = h2d_peak(bufs, bases if not cfg.scatter else {p: torch.empty(min(4 << 30, idx.partitions[p].length),
                                                                           dtype=torch.uint8, device=dev) for p in parts},
                      torch)
     stream = torch.cuda.current_stream(gpu)
@@ -335,13 +341,29 @@ def main():
     kern_launches = rep["kernel_launches"]
     kern_bytes = rep["kernel_bytes"]
     roof = None
+    h2d = {"bound": "pcie", "achieved": payload_bytes / (ms_step * 1e-3) / 1e9, "peak": b_h2d, "unit": "GB/s",
+           "frac": payload_bytes / (ms_step * 1e-3) / 1e9 / b_h2d, "peak_methods": b_h2d_methods,
+           "what": "whole step (a1-a8) vs the copy engine's measured host->device peak on the same buffers"}
+    if args.mode in ("ce", "scatter_ce") and kern_launches:
+        # the step's kernel: K4 (CE) / K3 (SCATTER_CE) on each landed chunk, per-launch
+        # CUDA events recorded by the library on its kernel stream over the timed region
+        per_launch_bytes = kern_bytes / kern_launches * (2 if args.mode == "scatter_ce" else 1)
+        avg_ms = kern_ms / kern_launches
+        achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9
+        hbm = peaks().get("hbm_gbs", 6551.4)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "kernel": "materialise_tma_kernel<%s> (in pipeline)" %
+                ("checksum only" if args.mode == "ce" else "scatter+checksum"),
+                "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
+                "bytes_per_launch": per_launch_bytes,
+                "note": "grid = blocks per chunk (one CTA per 1 MiB block); runs beside the PCIe copies"}
     if args.mode in ("zerocopy", "scatter_zc") and kern_launches:
         # zero-copy kernel: every byte it reads crosses PCIe -> bound by the host link.
         # Launches on the S streams overlap, so the kernel's rate is its bytes per step
         # over the step's device time (the kernel is the only work in the step).
         achieved = kern_bytes / (ms_step * 1e-3) / 1e9
         roof = {"bound": "pcie", "achieved": achieved, "peak": b_h2d, "unit": "GB/s", "frac": achieved / b_h2d,
-                "traffic": None, "kernel": "materialise_kernel<store,check,host_src>",
+                "traffic": None, "kernel": "materialise_tma_kernel<store,check> (zero-copy host source)",
                 "launches_per_step": kern_launches, "avg_launch_ms": kern_ms / max(kern_launches, 1),
                 "peak_source": "cudaMemcpyAsync H2D from the same pinned buffer, 4 GiB, best of 5, this run"}
     standalone = None
@@ -372,7 +394,7 @@ def main():
                 "b_h2d_measured_GBps": b_h2d, "frac_h2d": (payload_bytes / (ms_step * 1e-3) / 1e9) / b_h2d,
                 "gpu_launches": int(rep["kernel_launches"]) * args.steps,
                 "copy_calls_per_step": int(rep["copy_calls"]),
-                "clocks": clocks, "e2e": e2e, "roofline": roof, "standalone_hbm": standalone,
+                "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_h2d": h2d, "standalone_hbm": standalone,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -345,6 +345,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
 
 }  // namespace
 
+__global__ void gate_spin_kernel(const uint32_t* flag, uint32_t value) {
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int32_t)(v - value) >= 0) return;
+    __nanosleep(2000);
+  }
+}
+
+cudaError_t launch_gate_spin(const uint32_t* flag, uint32_t value, cudaStream_t stream) {
+  gate_spin_kernel<<<1, 1, 0, stream>>>(flag, value);
+  return cudaGetLastError();
+}
+
 template <bool kStore, bool kCheck>
 static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream) {
   static bool configured = false;  // per template instance

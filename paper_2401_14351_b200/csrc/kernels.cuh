@@ -52,4 +52,8 @@ enum class MatKind : int {
 // Launch on `stream` with `grid` CTAs (grid-stride over tiles).  Returns cudaGetLastError().
 cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream);
 
+// One-thread kernel that spins (with backoff) until *flag >= value in wrap-around order;
+// fallback for stream gates where cuStreamWaitValue32 is unavailable.
+cudaError_t launch_gate_spin(const uint32_t* flag, uint32_t value, cudaStream_t stream);
+
 }  // namespace sllm

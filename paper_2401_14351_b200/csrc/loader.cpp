@@ -84,6 +84,7 @@ struct PartJob {
   uint64_t* d_cs = nullptr;
   unsigned long long* d_bad = nullptr;
   cudaEvent_t ev[4] = {};  // start, end, setup, origin
+  Gate gate;               // caller-stream gate (origin != nullptr)
   // results
   std::vector<uint64_t> h_cs;
   bool h_cs_valid = false;
@@ -326,16 +327,12 @@ static void run_job(sllm_load* L, PartJob& j) {
     for (auto& e : P.freed) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t s0 = P.xfer[0];
-  for (auto& e : j.ev) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
   const uint64_t nb = pr.n_blocks;
   const size_t seg_bytes = align_up(j.segs.size() * sizeof(Seg), 256);
   const size_t acc_bytes = align_up(std::max<uint64_t>(nb, 1) * sizeof(BlockAcc), 256);
   const size_t tab_bytes = align_up(std::max<uint64_t>(nb, 1) * 8, 256);
   const size_t total = seg_bytes + acc_bytes + 2 * tab_bytes + 256;
-  if (j.origin) {
-    SLLM_CUDA(cudaEventRecord(j.ev[3], j.origin));
-    SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[3], 0));
-  }
+  if (j.origin) SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[3], 0));  // recorded by sllm_load_start
   SLLM_CUDA(cudaMallocAsync(&j.scratch, total, s0));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
     void* st = nullptr;
@@ -409,7 +406,7 @@ static void run_job(sllm_load* L, PartJob& j) {
     SLLM_CUDA(cudaEventDestroy(e));  // destruction is deferred until the event completes
   }
   SLLM_CUDA(cudaEventRecord(j.ev[1], s0));
-  if (j.origin) SLLM_CUDA(cudaStreamWaitEvent(j.origin, j.ev[1], 0));
+  if (j.origin) gate_open_device(s0, j.gate);  // releases the caller's stream on the device
   j.t_issue_ns = now_ns() - t0;
   SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
   SLLM_CUDA(cudaMemcpy(&j.h_bad, j.d_bad, 8, cudaMemcpyDeviceToHost));
@@ -441,6 +438,7 @@ static void run_job_guarded(sllm_load* L, PartJob& j) {
     j.status = SLLM_E_INVALID;
     j.error = e.what();
   }
+  gate_open_host(j.gate);  // never leave the caller's stream waiting (success or failure)
 }
 
 }  // namespace sllm
@@ -528,6 +526,29 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
       if (g_busy.count(k)) fail(SLLM_E_BUSY, "destination is already being loaded");
     for (const void* k : keys) g_busy.insert(k);
     L->busy_keys = std::move(keys);
+  }
+  // Caller-stream ordering is fixed here, on the caller's thread, before returning: the
+  // load starts after work already queued on stream[p], and stream[p] waits for the load.
+  try {
+    for (auto& j : L->jobs) {
+      SLLM_CUDA(cudaSetDevice(j.gpu));
+      for (auto& e : j.ev) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
+      if (j.origin) {
+        SLLM_CUDA(cudaEventRecord(j.ev[3], j.origin));
+        j.gate = gate_acquire();
+        gate_wait(j.origin, j.gate);
+      }
+    }
+  } catch (...) {
+    std::lock_guard<std::mutex> g(g_busy_mu);
+    for (const void* k : L->busy_keys) g_busy.erase(k);
+    for (auto& j : L->jobs) {
+      gate_open_host(j.gate);
+      gate_release(j.gate);
+      for (auto& e : j.ev)
+        if (e) cudaEventDestroy(e);
+    }
+    throw;
   }
   for (auto& j : L->jobs) j.th = std::thread(run_job_guarded, L.get(), std::ref(j));
   return L.release();
@@ -638,6 +659,7 @@ void sllm_load_free_internal(sllm_load* L) {
     if (j.staging) cudaFreeAsync(j.staging, device_ctx(j.gpu).streams[0]);
     for (auto& e : j.ev)
       if (e) cudaEventDestroy(e);
+    gate_release(j.gate);
   }
   delete L;
 }
