@@ -389,20 +389,11 @@ def load_start(index: Index, sources: Dict[int, object], gpus: Dict[int, int], c
         gpu[p] = int(gpus[p])
     dst_base = None
     dst_tensor = None
-    tensors: Dict[str, object] = {}
-    tdt = _torch_dtypes()
-    infos = index.tensors
     if not cfg.scatter:
         dst_base = _ptr_array([bases[p].data_ptr() if p in (bases or {}) else None for p in range(n)])
-        for t in infos:
-            if t.partition in sources:
-                b = bases[t.partition]
-                tensors[t.name] = b[t.offset:t.offset + t.nbytes].view(tdt[t.dtype]).view(t.shape)
     else:
-        dst_tensor = _ptr_array([per_tensor[t.name].data_ptr() if t.partition in sources else None for t in infos])
-        for t in infos:
-            if t.partition in sources:
-                tensors[t.name] = per_tensor[t.name]
+        dst_tensor = _ptr_array([per_tensor[t.name].data_ptr() if t.partition in sources else None
+                                 for t in index.tensors])
     st = None
     if streams:
         st = _ptr_array([streams[p].cuda_stream if p in streams else None for p in range(n)])
@@ -410,6 +401,17 @@ def load_start(index: Index, sources: Dict[int, object], gpus: Dict[int, int], c
     ccfg = cfg.to_c()
     check(lib().sllm_load_start(index.handle, C.byref(ccfg), _ptr_array(src), gpu, dst_base, dst_tensor, st,
                                 comm.handle if comm else None, C.byref(out)))
+    # The tensor objects are built while the transfer runs (the inference
+    # process sets base + offset pointers before the data has arrived).
+    tensors: Dict[str, object] = {}
+    tdt = _torch_dtypes()
+    for t in index.tensors:
+        if t.partition in sources:
+            if not cfg.scatter:
+                b = bases[t.partition]
+                tensors[t.name] = b[t.offset:t.offset + t.nbytes].view(tdt[t.dtype]).view(t.shape)
+            else:
+                tensors[t.name] = per_tensor[t.name]
     return LoadResult(out, index, tensors, [dst_base, dst_tensor, st, bases, per_tensor, sources])
 
 
