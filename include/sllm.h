@@ -164,6 +164,13 @@ SLLM_API sllm_status sllm_chunk_count(uint64_t length, uint64_t chunk, uint64_t*
  * chunk-aligned slices; lo_hi receives 2*nranks values {lo_0, hi_0, lo_1, hi_1, ...}.
  * Slices are balanced in whole chunks; trailing slices may be empty. */
 SLLM_API sllm_status sllm_replica_slices(uint64_t length, uint64_t chunk, int32_t nranks, uint64_t* lo_hi);
+/* Fan-out round schedule (the one sllm_load_wait's replicated path executes): round r
+ * broadcasts, from every rank q, the r-th chunk of q's slice.  lo_hi receives 2*nranks
+ * values {lo_q, hi_q} (hi_q == lo_q: rank q sends nothing in this round); *n_rounds (may
+ * be NULL) receives the number of rounds, max over q of ceil(|slice_q| / chunk).
+ * SLLM_E_LOOKUP if round >= n_rounds. */
+SLLM_API sllm_status sllm_replica_round(uint64_t length, uint64_t chunk, int32_t nranks, uint64_t round,
+                                        uint64_t* lo_hi, uint64_t* n_rounds);
 
 /* ------------------------------------------------------------------------------------
  * Pinned host memory (the DRAM tier).  Page-locked, mapped into the

@@ -85,6 +85,7 @@ SIGNATURES = {
     "sllm_fletcher64_host": (S, [P, U64, C.POINTER(U64)]),
     "sllm_chunk_count": (S, [U64, U64, C.POINTER(U64)]),
     "sllm_replica_slices": (S, [U64, U64, C.c_int32, C.POINTER(U64)]),
+    "sllm_replica_round": (S, [U64, U64, C.c_int32, U64, C.POINTER(U64), C.POINTER(U64)]),
     "sllm_host_alloc": (S, [U64, C.c_int32, PP]),
     "sllm_host_free": (None, [P]),
     "sllm_host_register": (S, [P, U64]),

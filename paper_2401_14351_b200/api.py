@@ -209,6 +209,21 @@ def replica_slices(length: int, chunk: int, nranks: int) -> List[Tuple[int, int]
     return [(arr[2 * r], arr[2 * r + 1]) for r in range(nranks)]
 
 
+def replica_schedule(length: int, chunk: int, nranks: int) -> List[List[Tuple[int, int]]]:
+    """The fan-out rounds the replicated load executes: rounds[r][q] = (lo, hi) that rank
+    q broadcasts in round r (lo == hi: nothing)."""
+    arr = (C.c_uint64 * (2 * nranks))()
+    n = C.c_uint64()
+    if length == 0:
+        return []
+    check(lib().sllm_replica_round(length, chunk, nranks, 0, arr, C.byref(n)))
+    out = []
+    for r in range(n.value):
+        check(lib().sllm_replica_round(length, chunk, nranks, r, arr, None))
+        out.append([(arr[2 * q], arr[2 * q + 1]) for q in range(nranks)])
+    return out
+
+
 class HostBuffer:
     """Pinned, device-mapped host memory from sllm_host_alloc (the DRAM tier)."""
 

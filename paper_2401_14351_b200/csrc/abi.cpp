@@ -216,6 +216,25 @@ sllm_status sllm_replica_slices(uint64_t length, uint64_t chunk, int32_t nranks,
   });
 }
 
+sllm_status sllm_replica_round(uint64_t length, uint64_t chunk, int32_t nranks, uint64_t round, uint64_t* lo_hi,
+                               uint64_t* n_rounds) {
+  return guard([&] {
+    if (!chunk || nranks < 1 || !lo_hi) fail(SLLM_E_INVALID, "bad round arguments");
+    std::vector<uint64_t> sl(2 * (size_t)nranks);
+    if (sllm_replica_slices(length, chunk, nranks, sl.data()) != SLLM_OK) fail(SLLM_E_INVALID, "slice plan failed");
+    uint64_t rounds = 0;
+    for (int32_t q = 0; q < nranks; ++q) rounds = std::max(rounds, ceil_div(sl[2 * q + 1] - sl[2 * q], chunk));
+    if (n_rounds) *n_rounds = rounds;
+    if (round >= rounds) fail(SLLM_E_LOOKUP, "round out of range");
+    for (int32_t q = 0; q < nranks; ++q) {
+      uint64_t a = sl[2 * q] + round * chunk;
+      bool has = a < sl[2 * q + 1];
+      lo_hi[2 * q] = has ? a : 0;
+      lo_hi[2 * q + 1] = has ? std::min(a + chunk, sl[2 * q + 1]) : 0;
+    }
+  });
+}
+
 sllm_status sllm_host_alloc(uint64_t bytes, int32_t gpu, void** p) {
   return guard([&] {
     if (!p) fail(SLLM_E_INVALID, "null out");

@@ -364,29 +364,27 @@ static void run_job(sllm_load* L, PartJob& j) {
     // round is then broadcast from its owner over NVLink (grouped, one root per slice).
     const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
     std::vector<uint64_t> lohi(2 * R);
-    if (sllm_replica_slices(pr.length, C, R, lohi.data()) != SLLM_OK) fail(SLLM_E_INVALID, "slice plan failed");
     uint64_t rounds = 0;
-    for (int q = 0; q < R; ++q) rounds = std::max(rounds, ceil_div(lohi[2 * q + 1] - lohi[2 * q], C));
+    if (sllm_replica_round(pr.length, C, R, 0, lohi.data(), &rounds) != SLLM_OK && pr.length)
+      fail(SLLM_E_INVALID, "fan-out schedule failed");
     cudaEvent_t evk;
     SLLM_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
     cudaStream_t cs = dc.comm_stream;
     SLLM_CUDA(cudaStreamWaitEvent(cs, j.ev[2], 0));
     for (uint64_t r = 0; r < rounds; ++r) {
-      uint64_t lo = lohi[2 * me] + r * C;
-      if (lo < lohi[2 * me + 1]) {
-        uint64_t hi = std::min(lo + C, lohi[2 * me + 1]);
+      if (sllm_replica_round(pr.length, C, R, r, lohi.data(), nullptr) != SLLM_OK)
+        fail(SLLM_E_INVALID, "fan-out schedule failed");
+      std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
+      for (int q = 0; q < R; ++q) ranges[q] = {lohi[2 * q], lohi[2 * q + 1]};
+      if (ranges[me].second > ranges[me].first) {  // this rank's own chunk of the round: PCIe
+        const uint64_t lo = ranges[me].first, hi = ranges[me].second;
         cudaStream_t done = issue_chunk(idx, cfg, j, P, lo / C, lo, hi);
         SLLM_CUDA(cudaEventRecord(evk, done));
         SLLM_CUDA(cudaStreamWaitEvent(cs, evk, 0));
       }
-      std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
-      for (int q = 0; q < R; ++q) {
-        uint64_t a = lohi[2 * q] + r * C;
-        ranges[q] = a < lohi[2 * q + 1] ? std::pair<uint64_t, uint64_t>(a, std::min(a + C, lohi[2 * q + 1]))
-                                        : std::pair<uint64_t, uint64_t>(0, 0);
+      for (int q = 0; q < R; ++q)
         if (q != me && ranges[q].second > ranges[q].first) j.fanout += ranges[q].second - ranges[q].first;
-      }
-      nccl_bcast_group(L->comm, ranges, j.dst_base, cs);
+      nccl_bcast_group(L->comm, ranges, j.dst_base, cs);  // NVLink: every root's chunk to every rank
       if (cfg.verify && idx.block)
         for (int q = 0; q < R; ++q)
           if (q != me && ranges[q].second > ranges[q].first) verify_range(idx, cfg, j, ranges[q].first, ranges[q].second, cs);
