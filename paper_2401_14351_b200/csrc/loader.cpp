@@ -207,19 +207,20 @@ struct Pipe {
   cudaEvent_t copied = nullptr;            // chunk k landed (recorded, then waited at once)
   std::vector<cudaEvent_t> freed;          // SCATTER_CE: staging slot reusable
   int nslot = 0;
+  uint64_t slot_bytes = 0;                 // SCATTER_CE: one window of chunks
+  uint64_t window = 1;                     // chunks per submission (kernel launch)
 };
 
-static MatParams chunk_params(const sllm_index& idx, const sllm_load_config& cfg, const PartJob& j, uint64_t k,
-                              uint64_t lo, uint64_t hi) {
+static MatParams window_params(const sllm_index& idx, const sllm_load_config& cfg, const PartJob& j, uint64_t k0,
+                               uint64_t k1, uint64_t lo, uint64_t hi) {
   const bool check = cfg.verify && idx.block;
   MatParams mp{};
   mp.lo = lo;
   mp.hi = hi;
   mp.segs = j.d_segs;
-  mp.seg_begin = j.chunk_seg[k];
+  mp.seg_begin = j.chunk_seg[k0];
   const uint64_t nch = j.chunk_seg.size() - 1;
-  mp.seg_end = k + 1 < nch ? std::min<uint32_t>(j.chunk_seg[k + 1] + 1, (uint32_t)j.segs.size())
-                           : (uint32_t)j.segs.size();
+  mp.seg_end = k1 < nch ? std::min<uint32_t>(j.chunk_seg[k1] + 1, (uint32_t)j.segs.size()) : (uint32_t)j.segs.size();
   mp.tile = tile_for(idx);
   mp.block = idx.block ? idx.block : kTile;
   mp.part_len = idx.parts[j.p].length;
@@ -231,19 +232,60 @@ static MatParams chunk_params(const sllm_index& idx, const sllm_load_config& cfg
   return mp;
 }
 
-// Issue chunk k = [lo, hi) of job j.  Returns the stream whose completion means "chunk k
-// is in place and verified" (used by the fan-out to order the broadcast after it).
-static cudaStream_t issue_chunk(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, Pipe& P, uint64_t k,
-                                uint64_t lo, uint64_t hi) {
+// Copy chunks [k0, k1) (chunk k = partition bytes [k*C, min((k+1)*C, L))) from the pinned
+// source to dst + (k*C - lo) on stream xs: one cudaMemcpyBatchAsync for the whole window
+// when the runtime has it (one API call instead of k1-k0), else one cudaMemcpyAsync each.
+static void copy_window(PartJob& j, bool prof, uint8_t* dst, uint64_t lo, uint64_t k0, uint64_t k1, uint64_t C,
+                        uint64_t L, cudaStream_t xs) {
+  static std::atomic<int> batch_ok{1};
+  const uint64_t n = k1 - k0;
+  auto e = timed_begin(prof, xs);
+  if (n > 1 && batch_ok.load()) {
+    std::vector<void*> dsts(n), srcs(n);
+    std::vector<size_t> sizes(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t a = (k0 + i) * C, b = std::min(a + C, L);
+      dsts[i] = dst + (a - lo);
+      srcs[i] = const_cast<uint8_t*>(j.src + a);
+      sizes[i] = b - a;
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t zero = 0, fail_idx = 0;
+    cudaError_t r = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &zero, 1, &fail_idx, xs);
+    if (r == cudaSuccess) {
+      timed_end(e, j.cev, xs);
+      j.copies += 1;
+      return;
+    }
+    cudaGetLastError();
+    batch_ok = 0;  // not supported here: fall back for the rest of the process
+  }
+  for (uint64_t k = k0; k < k1; ++k) {
+    const uint64_t a = k * C, b = std::min(a + C, L);
+    SLLM_CUDA(cudaMemcpyAsync(dst + (a - lo), j.src + a, b - a, cudaMemcpyHostToDevice, xs));
+    j.copies++;
+  }
+  timed_end(e, j.cev, xs);
+}
+
+// Issue the window of chunks [k0, k1) of job j: the copy engine moves every chunk (one
+// batched submission), then ONE verify / scatter launch covers the window; zero-copy
+// modes issue one kernel for the window.  Returns the stream whose completion means
+// "the window is in place and verified" (the fan-out orders its broadcast after it).
+static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, Pipe& P, uint64_t w,
+                                 uint64_t k0, uint64_t k1) {
   const bool check = cfg.verify && idx.block;
   const bool prof = cfg.profile != 0;
   const int ctas = cfg.ctas > 0 ? cfg.ctas : default_ctas(cfg.mode);
-  MatParams mp = chunk_params(idx, cfg, j, k, lo, hi);
-  cudaStream_t xs = P.xfer[k % P.S];
+  const uint64_t C = cfg.chunk_bytes, L = idx.parts[j.p].length;
+  const uint64_t lo = k0 * C, hi = std::min(k1 * C, L);
+  MatParams mp = window_params(idx, cfg, j, k0, k1, lo, hi);
+  cudaStream_t xs = P.xfer[w % P.S];
   cudaStream_t done = xs;
   switch (cfg.mode) {
     case SLLM_MODE_CE:
-      copy_h2d(j, prof, j.dst_base + lo, j.src + lo, hi - lo, xs);
+      copy_window(j, prof, j.dst_base + lo, lo, k0, k1, C, L, xs);
       if (check) {
         SLLM_CUDA(cudaEventRecord(P.copied, xs));
         SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
@@ -262,10 +304,10 @@ static cudaStream_t issue_chunk(const sllm_index& idx, const sllm_load_config& c
       launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, xs);
       break;
     case SLLM_MODE_SCATTER_CE: {
-      const int slot = (int)(k % (uint64_t)P.nslot);
-      uint8_t* stage = j.staging + (uint64_t)slot * cfg.chunk_bytes;
-      if (k >= (uint64_t)P.nslot) SLLM_CUDA(cudaStreamWaitEvent(xs, P.freed[slot], 0));
-      copy_h2d(j, prof, stage, j.src + lo, hi - lo, xs);
+      const int slot = (int)(w % (uint64_t)P.nslot);
+      uint8_t* stage = j.staging + (uint64_t)slot * P.slot_bytes;
+      if (w >= (uint64_t)P.nslot) SLLM_CUDA(cudaStreamWaitEvent(xs, P.freed[slot], 0));
+      copy_window(j, prof, stage, lo, k0, k1, C, L, xs);
       SLLM_CUDA(cudaEventRecord(P.copied, xs));
       SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
       mp.src = stage;
@@ -279,7 +321,7 @@ static cudaStream_t issue_chunk(const sllm_index& idx, const sllm_load_config& c
     default:
       fail(SLLM_E_INVALID, "unknown mode");
   }
-  j.chunks++;
+  j.chunks += k1 - k0;
   j.transferred += hi - lo;
   return done;
 }
@@ -321,6 +363,11 @@ static void run_job(sllm_load* L, PartJob& j) {
   for (int s = 0; s < P.S; ++s) P.xfer[s] = dc.streams[s];
   P.kern = dc.kern_stream;
   P.nslot = std::max(3, P.S + 1);
+  // Chunks are the copy engine's transfer unit; kernels and copy submissions are
+  // grouped per window of >= kWindowBytes so small chunks do not make the host issue
+  // loop (one API call per chunk) the bottleneck.
+  P.window = cfg.fanout == SLLM_FANOUT_BCAST ? 1 : std::max<uint64_t>(1, kWindowBytes / cfg.chunk_bytes);
+  P.slot_bytes = P.window * cfg.chunk_bytes;
   SLLM_CUDA(cudaEventCreateWithFlags(&P.copied, cudaEventDisableTiming));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
     P.freed.resize(P.nslot);
@@ -336,7 +383,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   SLLM_CUDA(cudaMallocAsync(&j.scratch, total, s0));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
     void* st = nullptr;
-    SLLM_CUDA(cudaMallocAsync(&st, (size_t)P.nslot * cfg.chunk_bytes, s0));
+    SLLM_CUDA(cudaMallocAsync(&st, (size_t)P.nslot * P.slot_bytes, s0));
     j.staging = static_cast<uint8_t*>(st);
   }
   uint8_t* base = static_cast<uint8_t*>(j.scratch);
@@ -378,7 +425,8 @@ static void run_job(sllm_load* L, PartJob& j) {
       for (int q = 0; q < R; ++q) ranges[q] = {lohi[2 * q], lohi[2 * q + 1]};
       if (ranges[me].second > ranges[me].first) {  // this rank's own chunk of the round: PCIe
         const uint64_t lo = ranges[me].first, hi = ranges[me].second;
-        cudaStream_t done = issue_chunk(idx, cfg, j, P, lo / C, lo, hi);
+        (void)hi;
+        cudaStream_t done = issue_window(idx, cfg, j, P, r, lo / C, lo / C + 1);
         SLLM_CUDA(cudaEventRecord(evk, done));
         SLLM_CUDA(cudaStreamWaitEvent(cs, evk, 0));
       }
@@ -393,7 +441,8 @@ static void run_job(sllm_load* L, PartJob& j) {
     SLLM_CUDA(cudaEventDestroy(evk));
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
-    for (uint64_t k = 0; k < nch; ++k) issue_chunk(idx, cfg, j, P, k, k * C, std::min((k + 1) * C, pr.length));
+    for (uint64_t k0 = 0, w = 0; k0 < nch; k0 += P.window, ++w)
+      issue_window(idx, cfg, j, P, w, k0, std::min(k0 + P.window, nch));
   }
   // join every stream into s0, then let the caller's stream wait for the load
   for (cudaStream_t t : tails) {

@@ -129,7 +129,8 @@ def test_verify_off_still_exact():
     for mode in MODES:
         cfg = sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode, verify=False)
         res = sllm.load(idx, bufs, {0: 0}, cfg)
-        assert res.report["kernel_launches"] == (0 if mode == "ce" else res.report["chunks"])
+        # one kernel per 64 MiB window of chunks (none at all for CE without verification)
+        assert res.report["kernel_launches"] == (0 if mode == "ce" else -(-res.report["chunks"] // 64))
         check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
 
 
