@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-sample-gib", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-standalone", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="no per-launch CUDA events in the timed region")
     return ap.parse_args()
 
 
@@ -304,7 +305,7 @@ def main():
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for _ in range(args.steps):
-            res, ix = step(True)
+            res, ix = step(not args.no_profile)
             reports.append(res.wait())
             del res, ix
         end.record(stream)

@@ -230,7 +230,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   uint64_t* empty = full + kStages;
   __shared__ unsigned long long s_red[3][kConsumerWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t unit = kCheck ? p.block : (1ull << 20);  // a CTA owns whole units
+  // Work unit: a 1/split-th of a checksum block (a CTA owns whole units).  split > 1 lets
+  // a launch covering few blocks still spread over every SM; the partial sums of a
+  // block's units are then combined with atomics and finalised by its last unit.
+  const uint64_t blk = kCheck ? p.block : (1ull << 20);
+  const uint64_t unit = blk / p.split;
   const uint64_t u_first = p.lo / unit, u_end = (p.hi + unit - 1) / unit;
 
   if (threadIdx.x == 0) {
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           }
         }
         if (kCheck) {
-          const uint32_t i0 = (uint32_t)((x - u * unit) >> 2);
+          const uint32_t i0 = (uint32_t)((x - (u * unit / blk) * blk) >> 2);
           const unsigned long long s4 = (unsigned long long)val.x + val.y + val.z + val.w;
           A += s4;
           Bs += (unsigned long long)i0 * s4;
@@ -331,12 +335,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           SB += s_red[1][w];
           SC += s_red[2][w];
         }
-        const unsigned long long fa = fold(SA), fb = fold(SB), fc = fold(SC);
-        const unsigned long long nw = ((e - u * unit) >> 2) % kM;
-        const unsigned long long s2 = fold(fold(nw * fa) + (kM - fb) + (kM - fc));
-        const unsigned long long cs = (s2 << 32) | fa;
-        if (p.cs_out) p.cs_out[u] = cs;
-        if (p.expect && p.expect[u] != cs) atomicMin(p.bad, (unsigned long long)u);
+        unsigned long long fa = fold(SA), fb = fold(SB), fc = fold(SC);
+        const uint64_t j = u * unit / blk;
+        const uint64_t blen = min(blk, p.part_len - j * blk);
+        bool last = true;
+        if (p.split > 1) {  // combine this unit's partial sums with the block's other units
+          BlockAcc* acc = p.acc + j;
+          atomicAdd(&acc->a, fa);
+          atomicAdd(&acc->b, fb);
+          atomicAdd(&acc->c, fc);
+          __threadfence();
+          last = atomicAdd(&acc->tiles_done, 1ull) == (blen + unit - 1) / unit - 1;
+          if (last) {
+            __threadfence();
+            fa = fold(atomicAdd(&acc->a, 0ull));
+            fb = fold(atomicAdd(&acc->b, 0ull));
+            fc = fold(atomicAdd(&acc->c, 0ull));
+          }
+        }
+        if (last) {
+          const unsigned long long nw = (blen >> 2) % kM;
+          const unsigned long long s2 = fold(fold(nw * fa) + (kM - fb) + (kM - fc));
+          const unsigned long long cs = (s2 << 32) | fa;
+          if (p.cs_out) p.cs_out[j] = cs;
+          if (p.expect && p.expect[j] != cs) atomicMin(p.bad, (unsigned long long)j);
+        }
       }
       consumer_sync();
     }
@@ -368,10 +391,25 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const uint64_t unit = kCheck ? p.block : (1ull << 20);
+  // Split checksum blocks into up to 16 units of >= one stage (16 KiB) while the launch
+  // has fewer than two units per SM, so a 64 MiB window still covers every SM.
+  MatParams q = p;
+  const uint64_t blk = kCheck ? p.block : (1ull << 20);
+  static int sm_count[64] = {};  // per device, queried once
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& sms = sm_count[dev & 63];
+  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  q.split = 1;
+  const uint64_t blocks = (p.hi + blk - 1) / blk - p.lo / blk;
+  while (q.split < 16 && blocks * q.split < 2ull * sms && blk / (2 * q.split) >= kStageBytes &&
+         (blk / (2 * q.split)) % 16 == 0)
+    q.split *= 2;
+  if (!kCheck) q.split = 1;
+  const uint64_t unit = blk / q.split;
   const uint64_t units = (p.hi + unit - 1) / unit - p.lo / unit;
   if ((uint64_t)grid > units) grid = (int)units;
-  materialise_tma_kernel<kStore, kCheck><<<grid, kTmaThreads, kTmaSmem, stream>>>(p);
+  materialise_tma_kernel<kStore, kCheck><<<grid, kTmaThreads, kTmaSmem, stream>>>(q);
   return cudaGetLastError();
 }
 

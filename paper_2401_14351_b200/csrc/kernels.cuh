@@ -41,6 +41,7 @@ struct MatParams {
   unsigned long long* bad;   // min failing block index (init UINT64_MAX)
   int host_src;              // 1: src is host-mapped pinned memory (zero-copy over PCIe)
   int engine;                // 0: LDG/STG tiles; 1: TMA bulk copies through a shared-memory ring
+  uint32_t split;            // TMA engine: units per checksum block (set by the launcher)
 };
 
 enum class MatKind : int {
