@@ -345,7 +345,7 @@ def main():
     h2d = {"bound": "pcie", "achieved": payload_bytes / (ms_step * 1e-3) / 1e9, "peak": b_h2d, "unit": "GB/s",
            "frac": payload_bytes / (ms_step * 1e-3) / 1e9 / b_h2d, "peak_methods": b_h2d_methods,
            "what": "whole step (a1-a8) vs the copy engine's measured host->device peak on the same buffers"}
-    if args.mode in ("ce", "scatter_ce") and kern_launches:
+    if args.mode in ("ce", "scatter_ce") and kern_launches and kern_ms > 0:
         # the step's kernel: K4 (CE) / K3 (SCATTER_CE) on each landed chunk, per-launch
         # CUDA events recorded by the library on its kernel stream over the timed region
         per_launch_bytes = kern_bytes / kern_launches * (2 if args.mode == "scatter_ce" else 1)
@@ -358,7 +358,7 @@ def main():
                 "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
                 "bytes_per_launch": per_launch_bytes,
                 "note": "grid = blocks per chunk (one CTA per 1 MiB block); runs beside the PCIe copies"}
-    if args.mode in ("zerocopy", "scatter_zc") and kern_launches:
+    if args.mode in ("zerocopy", "scatter_zc") and kern_launches and kern_ms > 0:
         # zero-copy kernel: every byte it reads crosses PCIe -> bound by the host link.
         # Launches on the S streams overlap, so the kernel's rate is its bytes per step
         # over the step's device time (the kernel is the only work in the step).

@@ -280,9 +280,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
       cur = lo;
     }
     Seg sg = kStore ? p.segs[cur] : Seg{0, 0, nullptr, 0};
+    const uint64_t bstart = (u * unit / blk) * blk;  // first byte of this unit's checksum block
     unsigned long long A = 0, Bs = 0, Cs = 0;
     for (uint64_t off = a; off < e; off += kStageBytes) {
       const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
+      const uint32_t w0 = (uint32_t)((off - bstart) >> 2);  // block word index of the stage start
       mbar_wait(&full[stage], phase);
       const uint8_t* sb = smem + (size_t)stage * kStageBytes;
 #pragma unroll 4
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           }
         }
         if (kCheck) {
-          const uint32_t i0 = (uint32_t)((x - (u * unit / blk) * blk) >> 2);
+          const uint32_t i0 = w0 + (v >> 2);
           const unsigned long long s4 = (unsigned long long)val.x + val.y + val.z + val.w;
           A += s4;
           Bs += (unsigned long long)i0 * s4;
