@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  __shared__ unsigned long long s_red[3][kConsumerWarps];
+  __shared__ unsigned long long s_red[2][3][kConsumerWarps];  // double-buffered by unit parity
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Work unit: a 1/split-th of a checksum block (a CTA owns whole units).  split > 1 lets
   // a launch covering few blocks still spread over every SM; the partial sums of a
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
 
   const int ct = threadIdx.x - 32;  // consumer thread 0..255
   const int cw = warp - 1;
-  uint32_t stage = 0, phase = 0;
-  for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x) {
+  uint32_t stage = 0, phase = 0, par = 0;
+  for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x, par ^= 1) {
     const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
     // segment holding byte a (same search in every thread: uniform, L1-cached)
     uint32_t cur = p.seg_begin;
@@ -324,18 +324,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
         Cs += __shfl_xor_sync(0xffffffffu, Cs, o);
       }
       if (lane == 0) {
-        s_red[0][cw] = A;
-        s_red[1][cw] = Bs;
-        s_red[2][cw] = Cs;
+        s_red[par][0][cw] = A;
+        s_red[par][1][cw] = Bs;
+        s_red[par][2][cw] = Cs;
       }
-      consumer_sync();
+      consumer_sync();  // the other parity's slots are rewritten only after the next unit's sync
       if (ct == 0) {
         unsigned long long SA = 0, SB = 0, SC = 0;
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) {
-          SA += s_red[0][w];
-          SB += s_red[1][w];
-          SC += s_red[2][w];
+          SA += s_red[par][0][w];
+          SB += s_red[par][1][w];
+          SC += s_red[par][2][w];
         }
         unsigned long long fa = fold(SA), fb = fold(SB), fc = fold(SC);
         const uint64_t j = u * unit / blk;
@@ -363,7 +363,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           if (p.expect && p.expect[j] != cs) atomicMin(p.bad, (unsigned long long)j);
         }
       }
-      consumer_sync();
     }
   }
 }
@@ -384,6 +383,15 @@ cudaError_t launch_gate_spin(const uint32_t* flag, uint32_t value, cudaStream_t 
   return cudaGetLastError();
 }
 
+static int num_sms() {
+  static int sm_count[64] = {};  // per device, queried once
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& sms = sm_count[dev & 63];
+  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  return sms;
+}
+
 template <bool kStore, bool kCheck>
 static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream) {
   static bool configured = false;  // per template instance
@@ -397,11 +405,7 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
   // has fewer than two units per SM, so a 64 MiB window still covers every SM.
   MatParams q = p;
   const uint64_t blk = kCheck ? p.block : (1ull << 20);
-  static int sm_count[64] = {};  // per device, queried once
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int& sms = sm_count[dev & 63];
-  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  const int sms = num_sms();
   q.split = 1;
   const uint64_t blocks = (p.hi + blk - 1) / blk - p.lo / blk;
   while (q.split < 16 && blocks * q.split < 2ull * sms && blk / (2 * q.split) >= kStageBytes &&
@@ -417,7 +421,7 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
 
 cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream) {
   if (p.hi <= p.lo) return cudaSuccess;
-  if (grid < 1) grid = 1;
+  if (grid < 1) grid = num_sms();  // default: one CTA per SM
   if (p.engine == 1) {
     switch (kind) {
       case MatKind::kChecksumOnly: return launch_tma<false, true>(p, grid, stream);

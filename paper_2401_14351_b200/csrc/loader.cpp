@@ -159,12 +159,9 @@ static uint32_t tile_for(const sllm_index& idx) {
   return idx.block ? (uint32_t)std::min<uint64_t>(kTile, idx.block) : kTile;
 }
 
-static int default_ctas(int mode) {
-  switch (mode) {
-    case SLLM_MODE_ZEROCOPY: case SLLM_MODE_SCATTER_ZC: return 32;
-    default: return 64;
-  }
-}
+// 0 = one CTA per SM (resolved by launch_materialise): every window's kernel spreads
+// over the whole GPU, splitting checksum blocks across CTAs when a window is small.
+static int default_ctas(int /*mode*/) { return 0; }
 
 static std::pair<cudaEvent_t, cudaEvent_t> timed_begin(bool on, cudaStream_t st) {
   std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
@@ -344,7 +341,7 @@ static void verify_range(const sllm_index& idx, const sllm_load_config& cfg, Par
   mp.cs_out = j.d_cs;
   mp.bad = j.d_bad;
   mp.engine = cfg.engine == 2 ? 0 : 1;
-  launch(j, cfg.profile != 0, mp, MatKind::kChecksumOnly, cfg.ctas > 0 ? cfg.ctas : 64, st);
+  launch(j, cfg.profile != 0, mp, MatKind::kChecksumOnly, cfg.ctas > 0 ? cfg.ctas : 0, st);
 }
 
 static void run_job(sllm_load* L, PartJob& j) {
