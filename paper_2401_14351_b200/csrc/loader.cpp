@@ -206,6 +206,7 @@ struct Pipe {
   int nslot = 0;
   uint64_t slot_bytes = 0;                 // SCATTER_CE: one window of chunks
   uint64_t window = 1;                     // chunks per submission (kernel launch)
+  uint64_t v_k0 = 0, v_k1 = 0;             // CE: landed chunks not yet verified [v_k0, v_k1)
 };
 
 static MatParams window_params(const sllm_index& idx, const sllm_load_config& cfg, const PartJob& j, uint64_t k0,
@@ -271,7 +272,7 @@ static void copy_window(PartJob& j, bool prof, uint8_t* dst, uint64_t lo, uint64
 // modes issue one kernel for the window.  Returns the stream whose completion means
 // "the window is in place and verified" (the fan-out orders its broadcast after it).
 static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, Pipe& P, uint64_t w,
-                                 uint64_t k0, uint64_t k1) {
+                                 uint64_t k0, uint64_t k1, bool last) {
   const bool check = cfg.verify && idx.block;
   const bool prof = cfg.profile != 0;
   const int ctas = cfg.ctas > 0 ? cfg.ctas : default_ctas(cfg.mode);
@@ -286,10 +287,18 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
       if (check) {
         SLLM_CUDA(cudaEventRecord(P.copied, xs));
         SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
-        mp.src = j.dst_base;
-        mp.src_origin = 0;
-        mp.host_src = 0;
-        launch(j, prof, mp, MatKind::kChecksumOnly, ctas, P.kern);
+        // K4 runs per verification span (>= kVerifyBytes of landed windows, and at the
+        // end): fewer, larger launches that keep every SM busy; the copies never wait.
+        if (P.v_k1 == P.v_k0) P.v_k0 = k0;
+        P.v_k1 = k1;
+        if (last || (std::min(P.v_k1 * C, L) - P.v_k0 * C) >= kVerifyBytes) {
+          MatParams vp = window_params(idx, cfg, j, P.v_k0, P.v_k1, P.v_k0 * C, std::min(P.v_k1 * C, L));
+          vp.src = j.dst_base;
+          vp.src_origin = 0;
+          vp.host_src = 0;
+          launch(j, prof, vp, MatKind::kChecksumOnly, ctas, P.kern);
+          P.v_k0 = P.v_k1 = 0;
+        }
         done = P.kern;
       }
       break;
@@ -423,7 +432,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       if (ranges[me].second > ranges[me].first) {  // this rank's own chunk of the round: PCIe
         const uint64_t lo = ranges[me].first, hi = ranges[me].second;
         (void)hi;
-        cudaStream_t done = issue_window(idx, cfg, j, P, r, lo / C, lo / C + 1);
+        cudaStream_t done = issue_window(idx, cfg, j, P, r, lo / C, lo / C + 1, true);
         SLLM_CUDA(cudaEventRecord(evk, done));
         SLLM_CUDA(cudaStreamWaitEvent(cs, evk, 0));
       }
@@ -439,7 +448,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
     for (uint64_t k0 = 0, w = 0; k0 < nch; k0 += P.window, ++w)
-      issue_window(idx, cfg, j, P, w, k0, std::min(k0 + P.window, nch));
+      issue_window(idx, cfg, j, P, w, k0, std::min(k0 + P.window, nch), k0 + P.window >= nch);
   }
   // join every stream into s0, then let the caller's stream wait for the load
   for (cudaStream_t t : tails) {
