@@ -206,7 +206,7 @@ typedef struct {
   int32_t fanout;       /* sllm_fanout; BCAST requires a comm and a 1-partition index       */
   int32_t verify;       /* 1 = check every block's Fletcher-64 against the index            */
   int32_t ctas;         /* CTAs per kernel launch (0 = mode default)                        */
-  int32_t profile;      /* 1 = time every launch/copy with CUDA events (report t_*_ms_sum)  */
+  int32_t profile;      /* 1 = time every kernel launch with CUDA events, 2 = also copies    */
   int32_t engine;       /* kernel engine: 0 = default (TMA), 1 = TMA bulk-copy ring, 2 = LDG tiles */
   int32_t reserved;     /* must be 0                                                        */
 } sllm_load_config;

@@ -233,11 +233,11 @@ static MatParams window_params(const sllm_index& idx, const sllm_load_config& cf
 // Copy chunks [k0, k1) (chunk k = partition bytes [k*C, min((k+1)*C, L))) from the pinned
 // source to dst + (k*C - lo) on stream xs: one cudaMemcpyBatchAsync for the whole window
 // when the runtime has it (one API call instead of k1-k0), else one cudaMemcpyAsync each.
-static void copy_window(PartJob& j, bool prof, uint8_t* dst, uint64_t lo, uint64_t k0, uint64_t k1, uint64_t C,
+static void copy_window(PartJob& j, int prof, uint8_t* dst, uint64_t lo, uint64_t k0, uint64_t k1, uint64_t C,
                         uint64_t L, cudaStream_t xs) {
   static std::atomic<int> batch_ok{1};
   const uint64_t n = k1 - k0;
-  auto e = timed_begin(prof, xs);
+  auto e = timed_begin(prof >= 2, xs);  // copies are timed only at profile level 2
   if (n > 1 && batch_ok.load()) {
     std::vector<void*> dsts(n), srcs(n);
     std::vector<size_t> sizes(n);
@@ -274,7 +274,7 @@ static void copy_window(PartJob& j, bool prof, uint8_t* dst, uint64_t lo, uint64
 static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, Pipe& P, uint64_t w,
                                  uint64_t k0, uint64_t k1, bool last) {
   const bool check = cfg.verify && idx.block;
-  const bool prof = cfg.profile != 0;
+  const int prof = cfg.profile;
   const int ctas = cfg.ctas > 0 ? cfg.ctas : default_ctas(cfg.mode);
   const uint64_t C = cfg.chunk_bytes, L = idx.parts[j.p].length;
   const uint64_t lo = k0 * C, hi = std::min(k1 * C, L);
@@ -291,7 +291,9 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
         // end): fewer, larger launches that keep every SM busy; the copies never wait.
         if (P.v_k1 == P.v_k0) P.v_k0 = k0;
         P.v_k1 = k1;
-        if (last || (std::min(P.v_k1 * C, L) - P.v_k0 * C) >= kVerifyBytes) {
+        // (near the end every window is verified at once, so the tail after the last copy
+        // is one window's K4, not a whole span's)
+        if (last || (std::min(P.v_k1 * C, L) - P.v_k0 * C) >= kVerifyBytes || hi + kVerifyBytes >= L) {
           MatParams vp = window_params(idx, cfg, j, P.v_k0, P.v_k1, P.v_k0 * C, std::min(P.v_k1 * C, L));
           vp.src = j.dst_base;
           vp.src_origin = 0;
@@ -510,7 +512,7 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (cfg.n_streams == 0) cfg.n_streams = 2;
   if (cfg.n_streams < 1 || cfg.n_streams > kMaxStreams) fail(SLLM_E_INVALID, "n_streams must be in 1..8");
   if (cfg.mode < SLLM_MODE_CE || cfg.mode > SLLM_MODE_SCATTER_ZC) fail(SLLM_E_INVALID, "unknown mode");
-  if (cfg.profile != 0 && cfg.profile != 1) fail(SLLM_E_INVALID, "profile must be 0 or 1");
+  if (cfg.profile < 0 || cfg.profile > 2) fail(SLLM_E_INVALID, "profile must be 0, 1 or 2");
   if (cfg.engine < 0 || cfg.engine > 2) fail(SLLM_E_INVALID, "unknown kernel engine");
   if (cfg.reserved) fail(SLLM_E_INVALID, "reserved config field must be 0");
   if (cfg.chunk_bytes % tile_for(*idx)) fail(SLLM_E_INVALID, "chunk size must be a multiple of the 64 KiB work tile");
