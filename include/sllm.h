@@ -289,6 +289,26 @@ SLLM_API sllm_status sllm_load_block_checksums(const sllm_load* load, size_t p, 
 SLLM_API void sllm_load_free(sllm_load* load);
 
 /* ------------------------------------------------------------------------------------
+ * Cross-process tensor handles (the inference process
+ * "acquires the base addresses for each GPU (i.e., CUDA IPC handles) from the model
+ * manager" and computes base + offset).  The exporter (loader process) publishes each
+ * partition's device base; the importer maps it and builds its tensors from the index.
+ * ------------------------------------------------------------------------------------ */
+typedef struct {
+  uint8_t handle[64];  /* cudaIpcMemHandle_t of the allocation that holds the region       */
+  uint64_t offset;     /* region start minus that allocation's base                         */
+  uint64_t nbytes;     /* region length                                                     */
+  int32_t gpu;         /* CUDA ordinal of the exporting device                              */
+  int32_t reserved;
+} sllm_ipc_region;
+/* dev_ptr: device pointer inside a cudaMalloc'd allocation (e.g. a torch tensor). */
+SLLM_API sllm_status sllm_ipc_export(const void* dev_ptr, uint64_t nbytes, sllm_ipc_region* out);
+/* Map an exported region into this (other) process on region->gpu; *dev_ptr = its start.
+ * The mapping stays valid until sllm_ipc_close; the exporter must keep the memory alive. */
+SLLM_API sllm_status sllm_ipc_open(const sllm_ipc_region* region, void** dev_ptr);
+SLLM_API sllm_status sllm_ipc_close(void* dev_ptr);
+
+/* ------------------------------------------------------------------------------------
  * Device-resident helpers (the kernels on their own; used for HBM-roofline measurement
  * and by users who already hold partition bytes in device memory).
  * ------------------------------------------------------------------------------------ */

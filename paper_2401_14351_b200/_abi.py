@@ -60,6 +60,11 @@ class TensorHandle(C.Structure):
                 ("shape", C.c_int64 * MAX_NDIM), ("ptr", C.c_void_p), ("nbytes", C.c_uint64)]
 
 
+class IpcRegion(C.Structure):
+    _fields_ = [("handle", C.c_uint8 * 64), ("offset", C.c_uint64), ("nbytes", C.c_uint64), ("gpu", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
 P = C.c_void_p
 PP = C.POINTER(C.c_void_p)
 U64 = C.c_uint64
@@ -100,6 +105,9 @@ SIGNATURES = {
     "sllm_load_tensor": (S, [P, C.c_char_p, C.POINTER(TensorHandle)]),
     "sllm_load_block_checksums": (S, [P, C.c_size_t, C.POINTER(C.POINTER(U64))]),
     "sllm_load_free": (None, [P]),
+    "sllm_ipc_export": (S, [P, U64, C.POINTER(IpcRegion)]),
+    "sllm_ipc_open": (S, [C.POINTER(IpcRegion), PP]),
+    "sllm_ipc_close": (S, [P]),
     "sllm_block_checksums_device": (S, [P, U64, U64, P, C.c_int32, P]),
     "sllm_materialise_device": (S, [P, C.c_size_t, P, PP, C.c_int32, P, C.POINTER(U64)]),
 }

@@ -342,3 +342,28 @@ sllm_status sllm_materialise_device(const sllm_index* idx, size_t p, const void*
 }
 
 }  // extern "C"
+
+namespace sllm {
+void ipc_export(const void* ptr, uint64_t nbytes, sllm_ipc_region* out);
+void* ipc_open(const sllm_ipc_region* r);
+void ipc_close(void* p);
+}  // namespace sllm
+
+extern "C" {
+
+sllm_status sllm_ipc_export(const void* dev_ptr, uint64_t nbytes, sllm_ipc_region* out) {
+  return guard([&] { ipc_export(dev_ptr, nbytes, out); });
+}
+
+sllm_status sllm_ipc_open(const sllm_ipc_region* region, void** dev_ptr) {
+  return guard([&] {
+    if (!dev_ptr) fail(SLLM_E_INVALID, "null out");
+    *dev_ptr = ipc_open(region);
+  });
+}
+
+sllm_status sllm_ipc_close(void* dev_ptr) {
+  return guard([&] { ipc_close(dev_ptr); });
+}
+
+}  // extern "C"
