@@ -262,6 +262,17 @@ SLLM_API sllm_status sllm_load_start(const sllm_index* index, const sllm_load_co
                             void* const* dst_base, void* const* dst_tensor,
                             void* const* stream, sllm_comm* comm, sllm_load** out);
 
+/* Start loading straight from the partition files <dir>/part_<device>.bin -- the whole
+ * multi-tier pipeline SSD -> pinned DRAM -> GPU: `io_threads`
+ * (0 = 4) readers fill a ring of pinned 64 MiB slots from a process-wide pool
+ * with O_DIRECT reads, each slot's window is copied / verified / scattered exactly
+ * as in sllm_load_start, and a slot is refilled once the GPU has consumed it.
+ *   gpu[p] : CUDA ordinal for partition p, or < 0 to skip that partition.
+ *   other arguments as in sllm_load_start (no fan-out).  SLLM_E_IO names the file. */
+SLLM_API sllm_status sllm_load_files_start(const sllm_index* index, const sllm_load_config* cfg, const char* dir,
+                                           const int32_t* gpu, void* const* dst_base, void* const* dst_tensor,
+                                           void* const* stream, int32_t io_threads, sllm_load** out);
+
 /* Block until every chunk (and fan-out round) has landed and been verified.  Returns
  * SLLM_E_CHECKSUM with rep->bad_partition / rep->bad_block naming the first failing
  * block, or the first CUDA/NCCL error.  Idempotent (returns the same status again).

@@ -8,7 +8,7 @@ ctypes binding over it; see ``api`` for the Python surface.
 """
 from ._abi import SllmError, lib, LIB_PATH  # noqa: F401
 from .api import (Index, HostBuffer, LoadConfig, LoadResult, Comm, TensorInfo, PartitionInfo,  # noqa: F401
-                  allocate, block_checksums_device, chunk_count, convert, fletcher64, load, load_start,
+                  allocate, block_checksums_device, chunk_count, convert, fletcher64, load, load_files, load_start,
                   materialise_device, replica_slices, replica_schedule)
 
 __all__ = ["SllmError", "lib", "Index", "HostBuffer", "LoadConfig", "LoadResult", "Comm", "allocate", "load",

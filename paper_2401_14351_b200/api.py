@@ -430,6 +430,45 @@ def load_start(index: Index, sources: Dict[int, object], gpus: Dict[int, int], c
     return LoadResult(out, index, tensors, [dst_base, dst_tensor, st, bases, per_tensor, sources])
 
 
+def load_files(index: Index, directory: str, gpus: Dict[int, int], config: Optional[LoadConfig] = None,
+               io_threads: int = 0, wait: bool = True, stream_of_caller: bool = True,
+               bases: Optional[Dict[int, object]] = None, per_tensor: Optional[Dict[str, object]] = None) -> LoadResult:
+    """The full multi-tier pipeline from <directory>/part_<device>.bin (sllm_load_files_start):
+    O_DIRECT readers -> pinned slot ring -> GPU, for the partitions listed in ``gpus``."""
+    import torch
+    cfg = config or LoadConfig()
+    if bases is None and per_tensor is None:
+        bases, per_tensor = allocate(index, gpus, cfg.scatter, partitions=gpus.keys())
+    parts = index.partitions
+    n = len(parts)
+    gpu = (C.c_int32 * max(n, 1))(*([-1] * max(n, 1)))
+    for p, g in gpus.items():
+        gpu[p] = int(g)
+    dst_base = dst_tensor = None
+    if not cfg.scatter:
+        dst_base = _ptr_array([bases[p].data_ptr() if p in bases else None for p in range(n)])
+    else:
+        dst_tensor = _ptr_array([per_tensor[t.name].data_ptr() if t.partition in gpus else None for t in index.tensors])
+    streams = {p: torch.cuda.current_stream(gpus[p]) for p in gpus} if stream_of_caller else {}
+    st = _ptr_array([streams[p].cuda_stream if p in streams else None for p in range(n)]) if streams else None
+    out = C.c_void_p()
+    ccfg = cfg.to_c()
+    check(lib().sllm_load_files_start(index.handle, C.byref(ccfg), directory.encode(), gpu, dst_base, dst_tensor, st,
+                                      io_threads, C.byref(out)))
+    tensors: Dict[str, object] = {}
+    tdt = _torch_dtypes()
+    for t in index.tensors:
+        if t.partition in gpus:
+            if not cfg.scatter:
+                tensors[t.name] = bases[t.partition][t.offset:t.offset + t.nbytes].view(tdt[t.dtype]).view(t.shape)
+            else:
+                tensors[t.name] = per_tensor[t.name]
+    res = LoadResult(out, index, tensors, [dst_base, dst_tensor, st, bases, per_tensor, None])
+    if wait:
+        res.wait()
+    return res
+
+
 def load(index: Index, sources: Dict[int, object], gpus: Dict[int, int], config: Optional[LoadConfig] = None,
          wait: bool = True, comm: Optional[Comm] = None, stream_of_caller: bool = True) -> LoadResult:
     """Allocate destinations with torch, start the load and (by default) wait for it --

@@ -23,7 +23,7 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
 }  // namespace sllm
 
 sllm_load* sllm_load_create_internal(const sllm_index*, const sllm_load_config*, const void* const*, const int32_t*,
-                                     void* const*, void* const*, void* const*, sllm_comm*);
+                                     void* const*, void* const*, void* const*, sllm_comm*, const char*, int32_t);
 sllm_status sllm_load_wait_internal(sllm_load*, sllm_load_report*);
 void sllm_load_tensor_internal(const sllm_load*, const char*, sllm_tensor_handle*);
 void sllm_load_block_checksums_internal(sllm_load*, size_t, const uint64_t**);
@@ -295,7 +295,16 @@ sllm_status sllm_load_start(const sllm_index* idx, const sllm_load_config* cfg, 
                             sllm_comm* comm, sllm_load** out) {
   return guard([&] {
     if (!out) fail(SLLM_E_INVALID, "null out");
-    *out = sllm_load_create_internal(idx, cfg, host_src, gpu, dst_base, dst_tensor, stream, comm);
+    *out = sllm_load_create_internal(idx, cfg, host_src, gpu, dst_base, dst_tensor, stream, comm, nullptr, 0);
+  });
+}
+
+sllm_status sllm_load_files_start(const sllm_index* idx, const sllm_load_config* cfg, const char* dir, const int32_t* gpu,
+                                  void* const* dst_base, void* const* dst_tensor, void* const* stream, int32_t io_threads,
+                                  sllm_load** out) {
+  return guard([&] {
+    if (!out || !dir) fail(SLLM_E_INVALID, "null argument");
+    *out = sllm_load_create_internal(idx, cfg, nullptr, gpu, dst_base, dst_tensor, stream, nullptr, dir, io_threads);
   });
 }
 

@@ -71,6 +71,9 @@ struct PartJob {
   const uint8_t* src_dev = nullptr;  // its device-visible alias (zero-copy modes)
   uint8_t* dst_base = nullptr;
   cudaStream_t origin = nullptr;
+  std::string file;                  // file tier: <dir>/part_<device>.bin (else empty)
+  int io_threads = 0;
+  FileSourcePtr fsrc;                // file tier: reader threads + pinned slot ring
   // fan-out slice of this rank (whole partition when not replicated)
   uint64_t lo = 0, hi = 0;
   std::vector<Seg> segs;
@@ -233,8 +236,8 @@ static MatParams window_params(const sllm_index& idx, const sllm_load_config& cf
 // Copy chunks [k0, k1) (chunk k = partition bytes [k*C, min((k+1)*C, L))) from the pinned
 // source to dst + (k*C - lo) on stream xs: one cudaMemcpyBatchAsync for the whole window
 // when the runtime has it (one API call instead of k1-k0), else one cudaMemcpyAsync each.
-static void copy_window(PartJob& j, int prof, uint8_t* dst, uint64_t lo, uint64_t k0, uint64_t k1, uint64_t C,
-                        uint64_t L, cudaStream_t xs) {
+static void copy_window(PartJob& j, int prof, uint8_t* dst, const uint8_t* wsrc, uint64_t lo, uint64_t k0, uint64_t k1,
+                        uint64_t C, uint64_t L, cudaStream_t xs) {
   static std::atomic<int> batch_ok{1};
   const uint64_t n = k1 - k0;
   auto e = timed_begin(prof >= 2, xs);  // copies are timed only at profile level 2
@@ -244,7 +247,7 @@ static void copy_window(PartJob& j, int prof, uint8_t* dst, uint64_t lo, uint64_
     for (uint64_t i = 0; i < n; ++i) {
       const uint64_t a = (k0 + i) * C, b = std::min(a + C, L);
       dsts[i] = dst + (a - lo);
-      srcs[i] = const_cast<uint8_t*>(j.src + a);
+      srcs[i] = const_cast<uint8_t*>(wsrc + (a - lo));
       sizes[i] = b - a;
     }
     cudaMemcpyAttributes attr{};
@@ -261,7 +264,7 @@ static void copy_window(PartJob& j, int prof, uint8_t* dst, uint64_t lo, uint64_
   }
   for (uint64_t k = k0; k < k1; ++k) {
     const uint64_t a = k * C, b = std::min(a + C, L);
-    SLLM_CUDA(cudaMemcpyAsync(dst + (a - lo), j.src + a, b - a, cudaMemcpyHostToDevice, xs));
+    SLLM_CUDA(cudaMemcpyAsync(dst + (a - lo), wsrc + (a - lo), b - a, cudaMemcpyHostToDevice, xs));
     j.copies++;
   }
   timed_end(e, j.cev, xs);
@@ -281,9 +284,13 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
   MatParams mp = window_params(idx, cfg, j, k0, k1, lo, hi);
   cudaStream_t xs = P.xfer[w % P.S];
   cudaStream_t done = xs;
+  // Source of the window: the pinned partition, or (file tier) the pinned ring slot the
+  // storage readers filled with this window (UVA: the slot's device alias is its address).
+  const uint8_t* wsrc = j.fsrc ? file_source_window(*j.fsrc, w) : j.src + lo;
+  const uint8_t* wsrc_dev = j.fsrc ? wsrc : j.src_dev + lo;
   switch (cfg.mode) {
     case SLLM_MODE_CE:
-      copy_window(j, prof, j.dst_base + lo, lo, k0, k1, C, L, xs);
+      copy_window(j, prof, j.dst_base + lo, wsrc, lo, k0, k1, C, L, xs);
       if (check) {
         SLLM_CUDA(cudaEventRecord(P.copied, xs));
         SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
@@ -306,8 +313,8 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
       break;
     case SLLM_MODE_ZEROCOPY:
     case SLLM_MODE_SCATTER_ZC:
-      mp.src = j.src_dev;
-      mp.src_origin = 0;
+      mp.src = wsrc_dev;
+      mp.src_origin = lo;
       mp.host_src = 1;
       launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, xs);
       break;
@@ -315,7 +322,7 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
       const int slot = (int)(w % (uint64_t)P.nslot);
       uint8_t* stage = j.staging + (uint64_t)slot * P.slot_bytes;
       if (w >= (uint64_t)P.nslot) SLLM_CUDA(cudaStreamWaitEvent(xs, P.freed[slot], 0));
-      copy_window(j, prof, stage, lo, k0, k1, C, L, xs);
+      copy_window(j, prof, stage, wsrc, lo, k0, k1, C, L, xs);
       SLLM_CUDA(cudaEventRecord(P.copied, xs));
       SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
       mp.src = stage;
@@ -329,6 +336,7 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
     default:
       fail(SLLM_E_INVALID, "unknown mode");
   }
+  if (j.fsrc) file_source_consumed(*j.fsrc, w, xs);  // the slot is free once xs is past its reader
   j.chunks += k1 - k0;
   j.transferred += hi - lo;
   return done;
@@ -376,6 +384,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   // loop (one API call per chunk) the bottleneck.
   P.window = cfg.fanout == SLLM_FANOUT_BCAST ? 1 : std::max<uint64_t>(1, kWindowBytes / cfg.chunk_bytes);
   P.slot_bytes = P.window * cfg.chunk_bytes;
+  if (!j.file.empty()) j.fsrc = file_source_open(j.file, pr.length, P.window * cfg.chunk_bytes, j.io_threads, j.gpu);
   SLLM_CUDA(cudaEventCreateWithFlags(&P.copied, cudaEventDisableTiming));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
     P.freed.resize(P.nslot);
@@ -464,6 +473,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   if (j.origin) gate_open_device(s0, j.gate);  // releases the caller's stream on the device
   j.t_issue_ns = now_ns() - t0;
   SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
+  j.fsrc.reset();  // file tier: readers are done, slots go back to the pinned pool
   SLLM_CUDA(cudaMemcpy(&j.h_bad, j.d_bad, 8, cudaMemcpyDeviceToHost));
   SLLM_CUDA(cudaEventElapsedTime(&j.t_dev_ms, j.ev[0], j.ev[1]));
   for (auto* v : {&j.kev, &j.cev}) {
@@ -502,7 +512,7 @@ using namespace sllm;
 
 sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_config* cfg_in, const void* const* host_src,
                                      const int32_t* gpu, void* const* dst_base, void* const* dst_tensor,
-                                     void* const* stream, sllm_comm* comm) {
+                                     void* const* stream, sllm_comm* comm, const char* dir, int32_t io_threads) {
   if (!idx) fail(SLLM_E_INVALID, "null index");
   if (!idx->sealed) fail(SLLM_E_INVALID, "index is planned but not sealed");
   sllm_load_config cfg{};
@@ -526,7 +536,8 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   } else if (cfg.fanout != SLLM_FANOUT_NONE) {
     fail(SLLM_E_INVALID, "unknown fan-out");
   }
-  if (!host_src || !gpu) fail(SLLM_E_INVALID, "null host_src / gpu array");
+  if ((!host_src && !dir) || !gpu) fail(SLLM_E_INVALID, "null host_src / gpu array");
+  if (dir && cfg.fanout != SLLM_FANOUT_NONE) fail(SLLM_E_INVALID, "the file tier does not combine with the fan-out");
   if (scatter && !dst_tensor) fail(SLLM_E_INVALID, "scatter modes need dst_tensor");
   if (!scatter && !dst_base) fail(SLLM_E_INVALID, "contiguous modes need dst_base");
 
@@ -537,11 +548,16 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   L->t0 = std::chrono::steady_clock::now();
   if (scatter) L->dst_tensor.assign(dst_tensor, dst_tensor + idx->tensors.size());
   for (size_t p = 0; p < idx->parts.size(); ++p) {
-    if (!host_src[p]) continue;
+    if (dir ? gpu[p] < 0 : !host_src[p]) continue;
     PartJob j;
     j.p = p;
     j.gpu = gpu[p];
-    j.src = static_cast<const uint8_t*>(host_src[p]);
+    if (dir) {
+      j.file = std::string(dir) + "/part_" + std::to_string(idx->parts[p].device) + ".bin";
+      j.io_threads = io_threads;
+    } else {
+      j.src = static_cast<const uint8_t*>(host_src[p]);
+    }
     j.dst_base = dst_base ? static_cast<uint8_t*>(dst_base[p]) : nullptr;
     j.origin = stream ? static_cast<cudaStream_t>(stream[p]) : nullptr;
     if (!scatter && !j.dst_base) fail(SLLM_E_INVALID, "null dst_base for a loaded partition");
@@ -555,16 +571,18 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
           fail(SLLM_E_INVALID, "destination of '" + idx->tensors[ti].name + "' is not 16-byte aligned");
       }
     }
-    // the source must be page-locked host memory ("pinned memory ... DMA")
-    cudaPointerAttributes at{};
     SLLM_CUDA(cudaSetDevice(j.gpu));
-    if (cudaPointerGetAttributes(&at, j.src) != cudaSuccess || at.type != cudaMemoryTypeHost) {
-      cudaGetLastError();
-      fail(SLLM_E_INVALID, "partition source is not pinned host memory (use sllm_host_alloc / sllm_host_register)");
+    if (!dir) {
+      // the source must be page-locked host memory ("pinned memory ... DMA")
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, j.src) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        fail(SLLM_E_INVALID, "partition source is not pinned host memory (use sllm_host_alloc / sllm_host_register)");
+      }
+      j.src_dev = static_cast<const uint8_t*>(at.devicePointer);
+      if ((cfg.mode == SLLM_MODE_ZEROCOPY || cfg.mode == SLLM_MODE_SCATTER_ZC) && !j.src_dev)
+        fail(SLLM_E_INVALID, "zero-copy modes need host memory mapped into the device address space");
     }
-    j.src_dev = static_cast<const uint8_t*>(at.devicePointer);
-    if ((cfg.mode == SLLM_MODE_ZEROCOPY || cfg.mode == SLLM_MODE_SCATTER_ZC) && !j.src_dev)
-      fail(SLLM_E_INVALID, "zero-copy modes need host memory mapped into the device address space");
     build_segments(*idx, j, scatter, L->dst_tensor, cfg.chunk_bytes);
     L->jobs.push_back(std::move(j));
   }
