@@ -109,6 +109,19 @@ def peaks():
         return {}
 
 
+def ncu_traffic(mode, bytes_per_launch):
+    """`traffic` for the roofline: DRAM bytes per launch from the committed `ncu --set full`
+    capture of an in-pipeline launch (profiles/<round>/ncu_traffic_<mode>.json, written by
+    tools/ncu_traffic.py), scaled from the captured launch's algorithmic bytes to this
+    run's average launch.  None when no capture is committed for the mode."""
+    import glob
+    hits = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_traffic_{mode}.json")))
+    if not hits:
+        return None, None
+    cap = json.load(open(hits[-1]))
+    return cap["traffic_over_algorithmic"] * bytes_per_launch, os.path.relpath(hits[-1], ROOT)
+
+
 def run_reference(args, rank, world):
     """Reference arm = the CPU oracle as it stands (oracle/loader.py) on this box's host
     cores, each step a bounded sample of the same workload."""
@@ -165,11 +178,13 @@ def cpu_baseline(args, bufs, idx, inv, seed):
                       f"copy every tensor, recompute+compare 1 MiB Fletcher-64 blocks; {dt:.1f} s"}
 
 
-def h2d_peak(bufs, bases, torch, gib=4, reps=3):
-    """B_h2d(1): the copy engine's best host->device rate from the same pinned buffer into
+def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1):
+    """B_h2d(N): the copy engine's best host->device rate from the same pinned buffer into
     the same destination over >= 4 GiB: max of one 4 GiB
     cudaMemcpyAsync and back-to-back 64 MiB cudaMemcpyAsync calls on one stream, best of
-    `reps` each.  Returns (GB/s, {method: GB/s})."""
+    `reps` each.  Under torchrun every rep starts on a barrier so all N links (and the host
+    DRAM / PCIe switches they share) are loaded at once; the aggregate is N * bytes / the
+    slowest rank's time.  Returns (aggregate GB/s, {method: aggregate GB/s})."""
     p = sorted(bufs)[0]
     n = min(gib << 30, bufs[p].nbytes)
     src = bufs[p].torch()[:n]
@@ -180,12 +195,20 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=3):
         for _ in range(reps):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
             s.record()
             for o in range(0, n, piece):
                 dst[o:o + piece].copy_(src[o:o + piece], non_blocking=True)
             e.record()
             e.synchronize()
-            best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)
+            ms = s.elapsed_time(e)
+            if world > 1:
+                t = torch.tensor([ms], device=dst.device)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            best = max(best, world * n / (ms * 1e-3) / 1e9)
         out[name] = best
     return max(out.values()), out
 
@@ -281,7 +304,7 @@ def main():
 
     b_h2d, b_h2d_methods = h2d_peak(bufs, bases if not cfg.scatter else {p: torch.empty(min(4 << 30, idx.partitions[p].length),
                                                                           dtype=torch.uint8, device=dev) for p in parts},
-                     torch)
+                     torch, world=world)
     stream = torch.cuda.current_stream(gpu)
 
     def step(prof: bool):
@@ -342,8 +365,8 @@ def main():
     kern_launches = rep["kernel_launches"]
     kern_bytes = rep["kernel_bytes"]
     roof = None
-    h2d = {"bound": "pcie", "achieved": payload_bytes / (ms_step * 1e-3) / 1e9, "peak": b_h2d, "unit": "GB/s",
-           "frac": payload_bytes / (ms_step * 1e-3) / 1e9 / b_h2d, "peak_methods": b_h2d_methods,
+    h2d = {"bound": "pcie", "achieved": value, "peak": b_h2d, "unit": "GB/s",
+           "frac": value / b_h2d, "peak_methods": b_h2d_methods, "n_links": world,
            "what": "whole step (a1-a8) vs the copy engine's measured host->device peak on the same buffers"}
     if args.mode in ("ce", "scatter_ce") and kern_launches and kern_ms > 0:
         # the step's kernel: K4 (CE) / K3 (SCATTER_CE) on each landed chunk, per-launch
@@ -352,18 +375,22 @@ def main():
         avg_ms = kern_ms / kern_launches
         achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9
         hbm = peaks().get("hbm_gbs", 6551.4)
+        traffic, traffic_src = ncu_traffic(args.mode, per_launch_bytes)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "kernel": "materialise_tma_kernel<%s> (in pipeline)" %
+                "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": "materialise_tma_kernel<%s> (in pipeline)" %
                 ("checksum only" if args.mode == "ce" else "scatter+checksum"),
                 "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
                 "bytes_per_launch": per_launch_bytes,
-                "note": "grid = blocks per chunk (one CTA per 1 MiB block); runs beside the PCIe copies"}
+                "note": "one CTA per SM; each launch verifies a >= 512 MiB span of landed windows "
+                        "(1 MiB blocks split into equal units for wave balance) beside the PCIe copies"}
     if args.mode in ("zerocopy", "scatter_zc") and kern_launches and kern_ms > 0:
         # zero-copy kernel: every byte it reads crosses PCIe -> bound by the host link.
         # Launches on the S streams overlap, so the kernel's rate is its bytes per step
         # over the step's device time (the kernel is the only work in the step).
         achieved = kern_bytes / (ms_step * 1e-3) / 1e9
-        roof = {"bound": "pcie", "achieved": achieved, "peak": b_h2d, "unit": "GB/s", "frac": achieved / b_h2d,
+        roof = {"bound": "pcie", "achieved": achieved, "peak": b_h2d / world, "unit": "GB/s",
+                "frac": achieved / (b_h2d / world),
                 "traffic": None, "kernel": "materialise_tma_kernel<store,check> (zero-copy host source)",
                 "launches_per_step": kern_launches, "avg_launch_ms": kern_ms / max(kern_launches, 1),
                 "peak_source": "cudaMemcpyAsync H2D from the same pinned buffer, 4 GiB, best of 5, this run"}
@@ -392,7 +419,7 @@ def main():
                            "raw_bytes_per_gpu": raw_bytes, "verify": "fletcher64 per 1 MiB block, every block",
                            "l2": "inputs 13 GB >> 126 MB L2, no flush needed", "parallelism": f"sharded x{world}"},
                 "time_to_loaded_model_s": ms_step * 1e-3, "t_alloc_s": t_alloc, "t_setup_s": t_setup,
-                "b_h2d_measured_GBps": b_h2d, "frac_h2d": (payload_bytes / (ms_step * 1e-3) / 1e9) / b_h2d,
+                "b_h2d_measured_GBps": b_h2d, "frac_h2d": value / b_h2d,
                 "gpu_launches": int(rep["kernel_launches"]) * args.steps,
                 "copy_calls_per_step": int(rep["copy_calls"]),
                 "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_h2d": h2d, "standalone_hbm": standalone,

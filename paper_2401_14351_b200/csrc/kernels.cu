@@ -408,9 +408,16 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
   const int sms = num_sms();
   q.split = 1;
   const uint64_t blocks = (p.hi + blk - 1) / blk - p.lo / blk;
-  while (q.split < 16 && blocks * q.split < 2ull * sms && blk / (2 * q.split) >= kStageBytes &&
-         (blk / (2 * q.split)) % 16 == 0)
-    q.split *= 2;
+  auto can_halve = [&](uint32_t s) { return s < 16 && blk / (2 * s) >= kStageBytes && (blk / (2 * s)) % 16 == 0; };
+  while (can_halve(q.split) && blocks * q.split < 2ull * sms) q.split *= 2;
+  // Wave balance: a launch of U equal units on G CTAs takes ceil(U/G) unit-times, so keep
+  // halving the unit (down to 64 KiB) until U / (ceil(U/G) * G) >= 0.95 -- e.g. a 397-block
+  // verification span on 148 SMs runs 2.68 of 3 waves (89 %) at split 1, 97.5 % at split 4.
+  auto balance = [&](uint32_t s) {
+    const uint64_t U = blocks * s, G = (uint64_t)(grid < 1 ? sms : grid);
+    return (double)U / (double)(((U + G - 1) / G) * G);
+  };
+  while (can_halve(q.split) && blk / (2 * q.split) >= (64u << 10) && balance(q.split) < 0.95) q.split *= 2;
   if (!kCheck) q.split = 1;
   const uint64_t unit = blk / q.split;
   const uint64_t units = (p.hi + unit - 1) / unit - p.lo / unit;

@@ -294,13 +294,14 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
       if (check) {
         SLLM_CUDA(cudaEventRecord(P.copied, xs));
         SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
-        // K4 runs per verification span (>= kVerifyBytes of landed windows, and at the
-        // end): fewer, larger launches that keep every SM busy; the copies never wait.
+        // K4 runs per verification span of landed windows: up to kVerifyBytes per launch
+        // (few, long launches that keep every SM streaming), and once the pending span is
+        // at least as long as what is still to come, at once -- spans halve towards the end,
+        // so the tail after the last copy is about one window's K4.  The copies never wait.
         if (P.v_k1 == P.v_k0) P.v_k0 = k0;
         P.v_k1 = k1;
-        // (near the end every window is verified at once, so the tail after the last copy
-        // is one window's K4, not a whole span's)
-        if (last || (std::min(P.v_k1 * C, L) - P.v_k0 * C) >= kVerifyBytes || hi + kVerifyBytes >= L) {
+        const uint64_t pending = std::min(P.v_k1 * C, L) - P.v_k0 * C;
+        if (last || pending >= kVerifyBytes || pending >= L - hi) {
           MatParams vp = window_params(idx, cfg, j, P.v_k0, P.v_k1, P.v_k0 * C, std::min(P.v_k1 * C, L));
           vp.src = j.dst_base;
           vp.src_origin = 0;

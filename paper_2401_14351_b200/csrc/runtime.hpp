@@ -22,7 +22,7 @@ namespace sllm {
 constexpr int kMaxStreams = 8;
 constexpr uint32_t kTile = 64u << 10;  // bytes per kernel work tile
 constexpr uint64_t kWindowBytes = 64ull << 20;   // min bytes per copy submission / kernel launch
-constexpr uint64_t kVerifyBytes = 512ull << 20;  // CE mode: min bytes per verification launch
+constexpr uint64_t kVerifyBytes = 2048ull << 20;  // CE mode: max bytes per verification launch
 
 // Library-owned, per-GPU resources reused across loads (no allocation in the hot path).
 struct DeviceCtx {
