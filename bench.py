@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--chunk-mib", type=int, default=64)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--fanout", default="none", choices=["none", "bcast", "p2p"],
+                    help="replicated checkpoint: every rank ends with a full replica; rank r reads slice r over "
+                         "PCIe and the rest arrives over NVLink (bcast: NCCL broadcasts, p2p: fused peer stores)")
     ap.add_argument("--cpu-sample-gib", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-standalone", action="store_true")
@@ -285,6 +288,9 @@ def main():
     # ---- setup (untimed): synthetic checkpoint packed into pinned DRAM by the converter
     t0 = time.perf_counter()
     inv, seed = models.model_inventory(args.config)
+    replicated = args.fanout != "none"
+    if replicated and len(set(t.device for t in inv)) != 1:
+        raise SystemExit("--fanout needs a single-partition (replicated) checkpoint config")
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=[0] if world == 1 or
                                        len(set(t.device for t in inv)) == 1 else [rank], gpu_of={0: gpu, rank: gpu})
     t_setup = time.perf_counter() - t0
@@ -292,7 +298,7 @@ def main():
     parts = sorted(bufs)
     gpus = {p: gpu for p in parts}
     cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, n_streams=args.streams, mode=args.mode,
-                          ctas=args.ctas, profile=True)
+                          ctas=args.ctas, profile=True, fanout=args.fanout)
     # a2: destination allocation (reported separately, Q19)
     torch.cuda.synchronize()
     ta = time.perf_counter()
@@ -306,11 +312,20 @@ def main():
                                                                           dtype=torch.uint8, device=dev) for p in parts},
                      torch, world=world)
     stream = torch.cuda.current_stream(gpu)
+    comm = None
+    if args.fanout == "p2p":      # peer group bound to every rank's replica (CUDA IPC over the process group)
+        if world > 1:
+            comm = sllm.Comm.peers_from_process_group(bases[0])
+        else:
+            sig = torch.zeros(2, dtype=torch.int32, device=dev)
+            comm = sllm.Comm.peers(1, 0, gpu, [bases[0].data_ptr()], [sig.data_ptr()], keep=[sig])
+    elif args.fanout == "bcast":  # NCCL communicator over the process group
+        comm = sllm.Comm.from_process_group(gpu) if world > 1 else sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, gpu)
 
     def step(prof: bool):
         c = sllm.LoadConfig(**{**cfg.__dict__, "profile": prof})
         ix = sllm.Index.from_bytes(blob)                  # a1: open + validate the index
-        res = sllm.load_start(ix, bufs, gpus, c, bases, per_tensor, {p: stream for p in parts})
+        res = sllm.load_start(ix, bufs, gpus, c, bases, per_tensor, {p: stream for p in parts}, comm)
         return res, ix
 
     for _ in range(args.warmup):
@@ -341,7 +356,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
+    # every rank ends the step with its own loaded model (sharded: its partition; replicated:
+    # a full replica, of which it moved 1/N over PCIe)
     value = payload_bytes * world / (ms_step * 1e-3) / 1e9
+    pcie_bytes = raw_bytes if not replicated else sum(r["transferred_bytes"] for r in reports) / len(reports)
 
     # ---- end-to-end through the public API (a2 allocation + index open + load + wait +
     #      D2H of the verification word), host wall clock, pinned sources
@@ -350,14 +368,26 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ix = sllm.Index.from_bytes(blob)
-        res = sllm.load(ix, bufs, gpus, sllm.LoadConfig(**{**cfg.__dict__, "profile": False}))
+        if comm is None:
+            res = sllm.load(ix, bufs, gpus, sllm.LoadConfig(**{**cfg.__dict__, "profile": False}))
+        else:  # a replicated group is bound to its replicas: no per-step allocation
+            res = sllm.load_start(ix, bufs, gpus, sllm.LoadConfig(**{**cfg.__dict__, "profile": False}), bases,
+                                  per_tensor, {p: stream for p in parts}, comm)
+            res.wait()
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t0)
         del res, ix
-    e2e = {"value": payload_bytes * world / min(e2e_t) / 1e9, "unit": "GB/s",
-           "h2d_bytes_per_step": raw_bytes + sum(idx.partitions[p].n_blocks * 8 for p in parts),
-           "d2h_bytes_per_step": 8 * len(parts), "includes": "torch allocation + index open + load + verify + wait",
-           "time_to_loaded_model_s": min(e2e_t)}
+    t_e2e = min(e2e_t)
+    if world > 1:  # the job's end-to-end time is its slowest rank's
+        t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e = {"value": payload_bytes * world / t_e2e / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": int(pcie_bytes) + sum(idx.partitions[p].n_blocks * 8 for p in parts),
+           "d2h_bytes_per_step": 8 * len(parts),
+           "includes": ("index open + load + verify + wait (replicas preallocated: the peer group is bound to them)"
+                        if comm is not None else "torch allocation + index open + load + verify + wait"),
+           "time_to_loaded_model_s": t_e2e}
 
     # ---- roofline of the dominant kernel, from the library's per-launch CUDA events
     rep = reports[-1]
@@ -365,9 +395,11 @@ def main():
     kern_launches = rep["kernel_launches"]
     kern_bytes = rep["kernel_bytes"]
     roof = None
-    h2d = {"bound": "pcie", "achieved": value, "peak": b_h2d, "unit": "GB/s",
-           "frac": value / b_h2d, "peak_methods": b_h2d_methods, "n_links": world,
-           "what": "whole step (a1-a8) vs the copy engine's measured host->device peak on the same buffers"}
+    pcie_rate = pcie_bytes * world / (ms_step * 1e-3) / 1e9
+    h2d = {"bound": "pcie", "achieved": pcie_rate, "peak": b_h2d, "unit": "GB/s",
+           "frac": pcie_rate / b_h2d, "peak_methods": b_h2d_methods, "n_links": world,
+           "what": "host->device bytes of the whole step (a1-a8) over its device time vs the copy engine's "
+                   "measured host->device peak on the same buffers (all links at once under torchrun)"}
     if args.mode in ("ce", "scatter_ce") and kern_launches and kern_ms > 0:
         # the step's kernel: K4 (CE) / K3 (SCATTER_CE) on each landed chunk, per-launch
         # CUDA events recorded by the library on its kernel stream over the timed region
@@ -382,7 +414,7 @@ def main():
                 ("checksum only" if args.mode == "ce" else "scatter+checksum"),
                 "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
                 "bytes_per_launch": per_launch_bytes,
-                "note": "one CTA per SM; each launch verifies a >= 512 MiB span of landed windows "
+                "note": "one CTA per SM; each launch verifies a span of landed windows (up to 2 GiB, halving towards the end) "
                         "(1 MiB blocks split into equal units for wave balance) beside the PCIe copies"}
     if args.mode in ("zerocopy", "scatter_zc") and kern_launches and kern_ms > 0:
         # zero-copy kernel: every byte it reads crosses PCIe -> bound by the host link.
@@ -414,17 +446,19 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {"workload": args.config, "mode": args.mode, "chunk_mib": args.chunk_mib,
+                "config": {"workload": args.config, "mode": args.mode, "fanout": args.fanout, "chunk_mib": args.chunk_mib,
                            "streams": args.streams, "ctas": args.ctas, "payload_bytes_per_gpu": payload_bytes,
                            "raw_bytes_per_gpu": raw_bytes, "verify": "fletcher64 per 1 MiB block, every block",
-                           "l2": "inputs 13 GB >> 126 MB L2, no flush needed", "parallelism": f"sharded x{world}"},
+                           "l2": "inputs 13 GB >> 126 MB L2, no flush needed", "parallelism": f"replicated x{world} ({args.fanout})" if replicated else f"sharded x{world}"},
                 "time_to_loaded_model_s": ms_step * 1e-3, "t_alloc_s": t_alloc, "t_setup_s": t_setup,
-                "b_h2d_measured_GBps": b_h2d, "frac_h2d": value / b_h2d,
+                "b_h2d_measured_GBps": b_h2d, "frac_h2d": pcie_rate / b_h2d,
                 "gpu_launches": int(rep["kernel_launches"]) * args.steps,
                 "copy_calls_per_step": int(rep["copy_calls"]),
                 "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_h2d": h2d, "standalone_hbm": standalone,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.free()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

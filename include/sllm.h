@@ -58,7 +58,8 @@ typedef enum {
   SLLM_E_NCCL = 8,        /* an NCCL call failed or libnccl could not be loaded                 */
   SLLM_E_CHECKSUM = 9,    /* a loaded block's Fletcher-64 differs from the index               */
   SLLM_E_BUSY = 10,       /* the destination set is already being loaded                 */
-  SLLM_E_NOMEM = 11       /* host allocation / pinning failed                                   */
+  SLLM_E_NOMEM = 11,      /* host allocation / pinning failed                                   */
+  SLLM_E_PEER = 12        /* P2P fan-out: a peer did not signal completion within the timeout   */
 } sllm_status;
 
 /* dtype codes; widths F16/BF16 2, F32 4, I8/U8 1, I64 8. */
@@ -197,7 +198,16 @@ typedef enum {
   SLLM_MODE_SCATTER_ZC = 3  /* SM-issued host reads scattered straight into per-tensor buffers */
 } sllm_mode;
 
-typedef enum { SLLM_FANOUT_NONE = 0, SLLM_FANOUT_BCAST = 1 } sllm_fanout;
+/* Replicated checkpoint (one partition, every GPU gets a full replica): rank r of n moves
+ * only its slice (sllm_replica_slices) over its own PCIe link; the other GPUs receive it
+ *   BCAST : by grouped ncclBroadcast per chunk round over NVLink (sllm_comm_init_rank/_all);
+ *   P2P   : inside the loading kernel itself -- the zero-copy kernel (ZEROCOPY) or the
+ *           per-window verify kernel (CE) stores every 16-byte vector into the rank's own
+ *           replica and, over NVLink, into every peer replica at the same offset; then a
+ *           device-side signal/wait exchange (system-scope release/acquire flags) orders
+ *           the peers' stores before each rank verifies what it received
+ *           (sllm_comm_init_peers). */
+typedef enum { SLLM_FANOUT_NONE = 0, SLLM_FANOUT_BCAST = 1, SLLM_FANOUT_P2P = 2 } sllm_fanout;
 
 typedef struct {
   uint64_t chunk_bytes; /* multiple of the index block size (and of align); 0 = 16 MiB    */
@@ -236,6 +246,25 @@ typedef struct {
 SLLM_API sllm_status sllm_comm_unique_id(void* id128);
 SLLM_API sllm_status sllm_comm_init_rank(const void* id128, int32_t nranks, int32_t rank, int32_t gpu, sllm_comm** out);
 SLLM_API sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_comm** out /* n handles */);
+/* Peer group for SLLM_FANOUT_P2P (fan-out fused into the loading
+ * kernel over NVLink peer memory, no NCCL).  Collective: every rank of the group creates
+ * its handle with the same arrays and then issues the same sequence of P2P loads.
+ *   nranks        : 1..8 (one NVSwitch node); rank: this process's rank; gpu: its device.
+ *   peer_base[q]  : device pointer, valid in THIS process, to rank q's replica (>= L bytes,
+ *                   16-byte aligned): peer_base[rank] is this rank's own destination (it
+ *                   must be dst_base[0] of every P2P load), the others come from
+ *                   sllm_ipc_open of the peers' sllm_ipc_export (or plain pointers when
+ *                   the ranks share a process).  The group is bound to these replicas.
+ *   peer_signal[q]: device pointer (valid here) to rank q's signal array of 2*nranks
+ *                   uint32 words, zero-filled once before the first load and owned by rank
+ *                   q: ready[r] (rank r's stores into q's replica are complete for that
+ *                   epoch) and done[r] (rank r finished that load; its replica may be
+ *                   overwritten by the next one), so back-to-back loads need no host barrier.
+ *   timeout_ms    : how long a rank waits for its peers' completion signals before the
+ *                   load fails with SLLM_E_PEER (0 = 60000).
+ * The handle owns its streams; sllm_comm_free releases them (never the replicas). */
+SLLM_API sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
+                                          uint32_t* const* peer_signal, uint64_t timeout_ms, sllm_comm** out);
 SLLM_API void sllm_comm_free(sllm_comm* comm);
 
 /* Start loading (asynchronous: returns once worker threads are launched).
@@ -254,7 +283,10 @@ SLLM_API void sllm_comm_free(sllm_comm* comm);
  *                    ordered after work already queued on it, and the stream is made to
  *                    wait for the load's completion, so work queued on it after
  *                    sllm_load_start sees the loaded bytes.  NULL array/entry = no ordering.
- *   comm           : NULL unless cfg->fanout == SLLM_FANOUT_BCAST.
+ *   comm           : NULL unless cfg->fanout is BCAST (NCCL communicator) or P2P (peer
+ *                    group); with a fan-out, host_src[0] needs to hold (pinned) only the
+ *                    rank's own slice [lo_r, hi_r) of sllm_replica_slices: bytes outside
+ *                    it are never read.
  * Returns SLLM_E_BUSY if one of dst_base/dst_tensor is the target of an unfinished load.
  * Tensor contents are defined only after sllm_load_wait returns SLLM_OK (Q17). */
 SLLM_API sllm_status sllm_load_start(const sllm_index* index, const sllm_load_config* cfg,
@@ -314,7 +346,9 @@ typedef struct {
 } sllm_ipc_region;
 /* dev_ptr: device pointer inside a cudaMalloc'd allocation (e.g. a torch tensor). */
 SLLM_API sllm_status sllm_ipc_export(const void* dev_ptr, uint64_t nbytes, sllm_ipc_region* out);
-/* Map an exported region into this (other) process on region->gpu; *dev_ptr = its start.
+/* Map an exported region into this (other) process in the context of device region->gpu
+ * (the exporter's GPU as exported; set it to the importing GPU to reach a peer's memory
+ * over NVLink, e.g. for a P2P peer group); *dev_ptr = its start.
  * The mapping stays valid until sllm_ipc_close; the exporter must keep the memory alive. */
 SLLM_API sllm_status sllm_ipc_open(const sllm_ipc_region* region, void** dev_ptr);
 SLLM_API sllm_status sllm_ipc_close(void* dev_ptr);

@@ -14,11 +14,12 @@ LIB_PATH = os.path.join(HERE, "libsllm.so")
 MAX_NDIM = 8
 
 STATUS = {0: "OK", 1: "INVALID", 2: "CONVERSION", 3: "FORMAT", 4: "LOOKUP", 5: "CAPACITY", 6: "IO",
-          7: "CUDA", 8: "NCCL", 9: "CHECKSUM", 10: "BUSY", 11: "NOMEM"}
-OK, E_INVALID, E_CONVERSION, E_FORMAT, E_LOOKUP, E_CAPACITY, E_IO, E_CUDA, E_NCCL, E_CHECKSUM, E_BUSY, E_NOMEM = range(12)
+          7: "CUDA", 8: "NCCL", 9: "CHECKSUM", 10: "BUSY", 11: "NOMEM", 12: "PEER"}
+(OK, E_INVALID, E_CONVERSION, E_FORMAT, E_LOOKUP, E_CAPACITY, E_IO, E_CUDA, E_NCCL, E_CHECKSUM, E_BUSY, E_NOMEM,
+ E_PEER) = range(13)
 
 MODE_CE, MODE_ZEROCOPY, MODE_SCATTER_CE, MODE_SCATTER_ZC = range(4)
-FANOUT_NONE, FANOUT_BCAST = range(2)
+FANOUT_NONE, FANOUT_BCAST, FANOUT_P2P = range(3)
 DTYPE_CODE = {"f16": 0, "bf16": 1, "f32": 2, "i8": 3, "u8": 4, "i64": 5}
 DTYPE_NAME = {v: k for k, v in DTYPE_CODE.items()}
 
@@ -99,6 +100,7 @@ SIGNATURES = {
     "sllm_comm_unique_id": (S, [P]),
     "sllm_comm_init_rank": (S, [P, C.c_int32, C.c_int32, C.c_int32, PP]),
     "sllm_comm_init_all": (S, [C.POINTER(C.c_int32), C.c_int32, PP]),
+    "sllm_comm_init_peers": (S, [C.c_int32, C.c_int32, C.c_int32, PP, PP, U64, PP]),
     "sllm_comm_free": (None, [P]),
     "sllm_load_start": (S, [P, C.POINTER(LoadConfig), PP, C.POINTER(C.c_int32), PP, PP, PP, P, PP]),
     "sllm_load_files_start": (S, [P, C.POINTER(LoadConfig), C.c_char_p, C.POINTER(C.c_int32), PP, PP, PP, C.c_int32,

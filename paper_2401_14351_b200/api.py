@@ -263,7 +263,7 @@ class LoadConfig:
     chunk_bytes: int = 16 << 20   # P:1279 "16MB" (read as MiB, Q9)
     n_streams: int = 2
     mode: str = "ce"              # ce | zerocopy | scatter_ce | scatter_zc
-    fanout: str = "none"          # none | bcast
+    fanout: str = "none"          # none | bcast (NCCL) | p2p (fused NVLink stores)
     verify: bool = True
     ctas: int = 0
     profile: bool = False         # per-launch CUDA-event timing (bench roofline)
@@ -272,7 +272,7 @@ class LoadConfig:
     def to_c(self) -> _abi.LoadConfig:
         modes = {"ce": _abi.MODE_CE, "zerocopy": _abi.MODE_ZEROCOPY, "scatter_ce": _abi.MODE_SCATTER_CE,
                  "scatter_zc": _abi.MODE_SCATTER_ZC}
-        fan = {"none": _abi.FANOUT_NONE, "bcast": _abi.FANOUT_BCAST}
+        fan = {"none": _abi.FANOUT_NONE, "bcast": _abi.FANOUT_BCAST, "p2p": _abi.FANOUT_P2P}
         return _abi.LoadConfig(self.chunk_bytes, self.n_streams, modes[self.mode], fan[self.fanout],
                                int(self.verify), self.ctas, int(self.profile),
                                {"tma": 1, "ldg": 2}[self.engine], 0)
@@ -310,6 +310,47 @@ class Comm:
         dist.broadcast_object_list(obj, src=0, group=group)
         return cls.init_rank(obj[0], world, rank, gpu)
 
+    @classmethod
+    def peers(cls, nranks: int, rank: int, gpu: int, peer_bases: Sequence[int], peer_signals: Sequence[int],
+              timeout_ms: int = 0, keep: Optional[list] = None) -> "Comm":
+        """Peer group for fanout="p2p" (sllm_comm_init_peers): device pointers, valid in
+        this process, to every rank's replica and zero-filled signal array (2*nranks int32)."""
+        out = C.c_void_p()
+        check(lib().sllm_comm_init_peers(nranks, rank, gpu, _ptr_array(peer_bases), _ptr_array(peer_signals),
+                                         timeout_ms, C.byref(out)))
+        c = cls(out.value)
+        c._keep = keep or []
+        return c
+
+    @classmethod
+    def peers_from_process_group(cls, base, group=None, timeout_ms: int = 0) -> "Comm":
+        """Collective over a torch.distributed group: export this rank's replica ``base`` (a
+        CUDA uint8 tensor) and a fresh signal array with CUDA IPC, exchange the handles
+        through the group, map the peers' and build the peer group."""
+        import torch
+        import torch.distributed as dist
+        from . import ipc
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        gpu = base.device.index
+        sig = torch.zeros(2 * world, dtype=torch.int32, device=base.device)
+        torch.cuda.synchronize(gpu)
+        mine = (ipc.export_region(base.data_ptr(), base.numel()), ipc.export_region(sig.data_ptr(), sig.numel() * 4))
+        regions = [None] * world
+        dist.all_gather_object(regions, mine, group=group)
+        bases, sigs, opened = [], [], []
+        for q, (rb, rs) in enumerate(regions):
+            if q == rank:
+                bases.append(base.data_ptr())
+                sigs.append(sig.data_ptr())
+            else:
+                pb, ps = ipc.open_region(rb, gpu), ipc.open_region(rs, gpu)
+                opened += [pb, ps]
+                bases.append(pb)
+                sigs.append(ps)
+        c = cls.peers(world, rank, gpu, bases, sigs, timeout_ms, keep=[base, sig])
+        c._opened = opened
+        return c
+
     @property
     def handle(self):
         return self._h
@@ -318,6 +359,10 @@ class Comm:
         if self._h and self._h.value:
             lib().sllm_comm_free(self._h)
             self._h = C.c_void_p()
+        from . import ipc
+        for p in getattr(self, "_opened", []):
+            ipc.close(p)
+        self._opened = []
 
     def __del__(self):
         try:

@@ -31,6 +31,7 @@ void sllm_load_free_internal(sllm_load*);
 void sllm_comm_unique_id_internal(void*);
 sllm_comm* sllm_comm_init_rank_internal(const void*, int32_t, int32_t, int32_t);
 void sllm_comm_init_all_internal(const int32_t*, int32_t, sllm_comm**);
+sllm_comm* sllm_comm_init_peers_internal(int32_t, int32_t, int32_t, void* const*, uint32_t* const*, uint64_t);
 void sllm_comm_free_internal(sllm_comm*);
 
 using namespace sllm;
@@ -284,6 +285,14 @@ sllm_status sllm_comm_init_rank(const void* id128, int32_t nranks, int32_t rank,
 
 sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_comm** out) {
   return guard([&] { sllm_comm_init_all_internal(gpus, n, out); });
+}
+
+sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
+                                 uint32_t* const* peer_signal, uint64_t timeout_ms, sllm_comm** out) {
+  return guard([&] {
+    if (!out) fail(SLLM_E_INVALID, "null out");
+    *out = sllm_comm_init_peers_internal(nranks, rank, gpu, peer_base, peer_signal, timeout_ms);
+  });
 }
 
 void sllm_comm_free(sllm_comm* c) {

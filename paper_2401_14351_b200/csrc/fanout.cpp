@@ -63,8 +63,17 @@ static void nccl_check(ncclResult_t r, const char* what) {
 }  // namespace sllm
 
 struct sllm_comm {
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;  // NCCL communicator (SLLM_FANOUT_BCAST)
   int nranks = 0, rank = 0, dev = 0;
+  // peer group (SLLM_FANOUT_P2P): every rank's replica base and signal array, as device
+  // pointers valid in this process; streams owned by the group so that several ranks on
+  // one GPU (tests) never queue behind each other's peer waits
+  bool peers = false;
+  std::vector<uint8_t*> base;
+  std::vector<uint32_t*> signal;
+  uint32_t epoch = 0;
+  uint64_t timeout_ns = 0;
+  cudaStream_t streams[sllm::kMaxStreams + 1] = {};
 };
 
 namespace sllm {
@@ -72,6 +81,18 @@ namespace sllm {
 int comm_nranks(const sllm_comm* c) { return c->nranks; }
 int comm_rank(const sllm_comm* c) { return c->rank; }
 int comm_device(const sllm_comm* c) { return c->dev; }
+bool comm_is_peers(const sllm_comm* c) { return c->peers; }
+uint8_t* comm_peer_base(const sllm_comm* c, int q) { return c->base[q]; }
+uint32_t* comm_peer_signal(const sllm_comm* c, int q) { return c->signal[q]; }
+uint64_t comm_timeout_ns(const sllm_comm* c) { return c->timeout_ns; }
+uint32_t comm_next_epoch(sllm_comm* c) {
+  if (++c->epoch == 0) ++c->epoch;  // 0 is the signal arrays' initial value
+  return c->epoch;
+}
+cudaStream_t comm_stream(sllm_comm* c, int s) {  // s = 0..kMaxStreams-1 transfer, kMaxStreams = kernel
+  if (!c->streams[s]) SLLM_CUDA(cudaStreamCreateWithFlags(&c->streams[s], cudaStreamNonBlocking));
+  return c->streams[s];
+}
 
 // One round: ranges_by_root[q] = [lo, hi) broadcast from rank q (empty = no message).
 void nccl_bcast_group(sllm_comm* c, const std::vector<std::pair<uint64_t, uint64_t>>& ranges, uint8_t* buf,
@@ -131,8 +152,52 @@ void sllm_comm_init_all_internal(const int32_t* gpus, int32_t n, sllm_comm** out
   }
 }
 
+// P2P peer group (no NCCL): SURVEY §8(f) rank 4 -- the fan-out fused into the loading
+// kernel, stores over NVLink straight into every peer's replica.
+sllm_comm* sllm_comm_init_peers_internal(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
+                                         uint32_t* const* peer_signal, uint64_t timeout_ms) {
+  if (nranks < 1 || nranks > kMaxPeers + 1 || rank < 0 || rank >= nranks || gpu < 0 || !peer_base || !peer_signal)
+    fail(SLLM_E_INVALID, "bad peer-group arguments (1 <= nranks <= 8, 0 <= rank < nranks)");
+  SLLM_CUDA(cudaSetDevice(gpu));
+  std::unique_ptr<sllm_comm> c(new sllm_comm);
+  c->nranks = nranks;
+  c->rank = rank;
+  c->dev = gpu;
+  c->peers = true;
+  c->timeout_ns = (timeout_ms ? timeout_ms : 60000ull) * 1000000ull;
+  for (int q = 0; q < nranks; ++q) {
+    if (!peer_base[q] || !peer_signal[q]) fail(SLLM_E_INVALID, "null peer base / signal");
+    if (reinterpret_cast<uintptr_t>(peer_base[q]) & 15) fail(SLLM_E_INVALID, "peer base must be 16-byte aligned");
+    if (reinterpret_cast<uintptr_t>(peer_signal[q]) & 3) fail(SLLM_E_INVALID, "peer signal must be 4-byte aligned");
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, peer_base[q]) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      fail(SLLM_E_INVALID, "peer base " + std::to_string(q) + " is not device memory visible to this process");
+    }
+    if (at.device != gpu) {  // a replica on another GPU: this GPU must be able to store into it
+      int ok = 0;
+      SLLM_CUDA(cudaDeviceCanAccessPeer(&ok, gpu, at.device));
+      if (!ok) fail(SLLM_E_INVALID, "GPU " + std::to_string(gpu) + " cannot access peer GPU " + std::to_string(at.device));
+      cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) SLLM_CUDA(e);
+      cudaGetLastError();
+    }
+    c->base.push_back(static_cast<uint8_t*>(peer_base[q]));
+    c->signal.push_back(peer_signal[q]);
+  }
+  return c.release();
+}
+
 void sllm_comm_free_internal(sllm_comm* c) {
   if (!c) return;
   if (c->comm && g_nccl_ok) g_nccl.CommDestroy(c->comm);
+  if (c->peers) {
+    cudaSetDevice(c->dev);
+    for (auto& s : c->streams)
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+  }
   delete c;
 }

@@ -293,11 +293,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
         const uint64_t x = off + v;
         if (kStore) {
           while (x >= sg.off + sg.len && cur + 1 < p.seg_end) sg = p.segs[++cur];
-          if (sg.dst) {
+          if (sg.dst && !p.no_seg_store) {
             const uint64_t rel = x - sg.off;
             if (rel + 16 <= sg.valid) store16(sg.dst + rel, val);
             else if (rel < sg.valid) store_partial(sg.dst + rel, val, (uint32_t)(sg.valid - rel));
           }
+          // P2P fan-out: the same vector to every peer replica (NVLink stores; partitions are
+          // multiples of the alignment >= 16, so whole vectors only)
+          for (uint32_t k = 0; k < p.n_peers; ++k) store16(p.peer[k] + x, val);
         }
         if (kCheck) {
           const uint32_t i0 = w0 + (v >> 2);
@@ -368,6 +371,48 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
 }
 
 }  // namespace
+
+__global__ void peer_signal_kernel(const PeerSignal s, uint32_t epoch) {
+  // every store of the preceding fan-out kernels (same stream) happens-before this
+  // kernel; the system-scope release makes them visible to a peer that acquires the flag
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (uint32_t k = threadIdx.x; k < s.n; k += blockDim.x)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(s.remote[k]), "r"(epoch) : "memory");
+}
+
+__global__ void peer_wait_kernel(const uint32_t* own, int nranks, int me, uint32_t epoch, uint64_t timeout_ns,
+                                 uint32_t* err) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int q = 0; q < nranks; ++q) {
+    if (q == me) continue;
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(own + q) : "memory");
+      if ((int32_t)(v - epoch) >= 0) break;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        *err = 1u + (uint32_t)q;
+        return;
+      }
+      __nanosleep(1000);
+    }
+  }
+}
+
+cudaError_t launch_peer_signal(const PeerSignal& s, uint32_t epoch, cudaStream_t stream) {
+  if (!s.n) return cudaSuccess;
+  peer_signal_kernel<<<1, 32, 0, stream>>>(s, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const uint32_t* own, int nranks, int me, uint32_t epoch, uint64_t timeout_ns,
+                             uint32_t* err, cudaStream_t stream) {
+  if (nranks <= 1) return cudaSuccess;
+  peer_wait_kernel<<<1, 1, 0, stream>>>(own, nranks, me, epoch, timeout_ns, err);
+  return cudaGetLastError();
+}
 
 __global__ void gate_spin_kernel(const uint32_t* flag, uint32_t value) {
   for (;;) {

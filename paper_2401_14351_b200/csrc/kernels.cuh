@@ -25,6 +25,8 @@ struct BlockAcc {
   unsigned long long a, b, c, tiles_done;
 };
 
+constexpr int kMaxPeers = 7;  // P2P fan-out: up to 8 GPUs (an NVSwitch node)
+
 // One launch of the materialise/checksum kernel covers partition bytes [lo, hi).
 struct MatParams {
   const uint8_t* src;        // address holding partition byte `src_origin` (host-mapped or device)
@@ -42,6 +44,13 @@ struct MatParams {
   int host_src;              // 1: src is host-mapped pinned memory (zero-copy over PCIe)
   int engine;                // 0: LDG/STG tiles; 1: TMA bulk copies through a shared-memory ring
   uint32_t split;            // TMA engine: units per checksum block (set by the launcher)
+  // P2P fan-out (TMA engine, contiguous single segment): every stored vector of partition
+  // offset x also goes to peer[k] + x -- device pointers to the other GPUs' replicas,
+  // written over NVLink -- and, with no_seg_store, only there (CE: the source is the
+  // rank's own replica, already in place).
+  uint32_t n_peers;
+  uint32_t no_seg_store;
+  uint8_t* peer[kMaxPeers];
 };
 
 enum class MatKind : int {
@@ -52,6 +61,19 @@ enum class MatKind : int {
 
 // Launch on `stream` with `grid` CTAs (grid-stride over tiles).  Returns cudaGetLastError().
 cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream);
+
+// P2P fan-out completion: publish `epoch` into one slot of every peer's
+// signal array (system-scope release, after every store of the preceding kernels), and
+// wait until every peer has published at least `epoch` into this GPU's own array
+// (system-scope acquire).  A peer that has not signalled after timeout_ns sets
+// *err = 1 + its rank and the wait returns (no hang).
+struct PeerSignal {
+  uint32_t* remote[kMaxPeers];  // &signal_q[me] for every peer q
+  uint32_t n;
+};
+cudaError_t launch_peer_signal(const PeerSignal& s, uint32_t epoch, cudaStream_t stream);
+cudaError_t launch_peer_wait(const uint32_t* own, int nranks, int me, uint32_t epoch, uint64_t timeout_ns,
+                             uint32_t* err, cudaStream_t stream);
 
 // One-thread kernel that spins (with backoff) until *flag >= value in wrap-around order;
 // fallback for stream gates where cuStreamWaitValue32 is unavailable.

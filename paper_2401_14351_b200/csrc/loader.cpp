@@ -76,6 +76,12 @@ struct PartJob {
   FileSourcePtr fsrc;                // file tier: reader threads + pinned slot ring
   // fan-out slice of this rank (whole partition when not replicated)
   uint64_t lo = 0, hi = 0;
+  // P2P fan-out: the peers' replicas (device pointers valid here), this load's epoch
+  uint8_t* peers[kMaxPeers] = {};
+  uint32_t n_peers = 0;
+  uint32_t epoch = 0;
+  uint32_t h_err = 0;                // peer-wait result (0 = every peer signalled)
+  uint32_t* d_err = nullptr;
   std::vector<Seg> segs;
   std::vector<uint32_t> chunk_seg;  // first segment of each chunk of [0, L)
   // device scratch (one cudaMallocAsync block)
@@ -230,6 +236,8 @@ static MatParams window_params(const sllm_index& idx, const sllm_load_config& cf
   mp.cs_out = check ? j.d_cs : nullptr;
   mp.bad = j.d_bad;
   mp.engine = cfg.engine == 2 ? 0 : 1;
+  mp.n_peers = j.n_peers;
+  for (uint32_t k = 0; k < j.n_peers; ++k) mp.peer[k] = j.peers[k];
   return mp;
 }
 
@@ -291,7 +299,18 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
   switch (cfg.mode) {
     case SLLM_MODE_CE:
       copy_window(j, prof, j.dst_base + lo, wsrc, lo, k0, k1, C, L, xs);
-      if (check) {
+      if (j.n_peers) {
+        // P2P fan-out: one kernel per landed window reads it back from the rank's own
+        // replica, verifies it and stores it into every peer replica over NVLink
+        SLLM_CUDA(cudaEventRecord(P.copied, xs));
+        SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
+        mp.src = j.dst_base;
+        mp.src_origin = 0;
+        mp.host_src = 0;
+        mp.no_seg_store = 1;
+        launch(j, prof, mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas, P.kern);
+        done = P.kern;
+      } else if (check) {
         SLLM_CUDA(cudaEventRecord(P.copied, xs));
         SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
         // K4 runs per verification span of landed windows: up to kVerifyBytes per launch
@@ -314,6 +333,7 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
       break;
     case SLLM_MODE_ZEROCOPY:
     case SLLM_MODE_SCATTER_ZC:
+      // (P2P fan-out: the same kernel also stores every vector into the peer replicas)
       mp.src = wsrc_dev;
       mp.src_origin = lo;
       mp.host_src = 1;
@@ -364,6 +384,17 @@ static void verify_range(const sllm_index& idx, const sllm_load_config& cfg, Par
   launch(j, cfg.profile != 0, mp, MatKind::kChecksumOnly, cfg.ctas > 0 ? cfg.ctas : 0, st);
 }
 
+// s0 waits for the work queued so far on every stream of `tails`.
+static void join_streams(const std::vector<cudaStream_t>& tails, cudaStream_t s0) {
+  for (cudaStream_t t : tails) {
+    cudaEvent_t e;
+    SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SLLM_CUDA(cudaEventRecord(e, t));
+    SLLM_CUDA(cudaStreamWaitEvent(s0, e, 0));
+    SLLM_CUDA(cudaEventDestroy(e));  // destruction is deferred until the event completes
+  }
+}
+
 static void run_job(sllm_load* L, PartJob& j) {
   const sllm_index& idx = *L->idx;
   const sllm_load_config& cfg = L->cfg;
@@ -377,8 +408,9 @@ static void run_job(sllm_load* L, PartJob& j) {
   }
   Pipe P;
   P.S = cfg.n_streams;
-  for (int s = 0; s < P.S; ++s) P.xfer[s] = dc.streams[s];
-  P.kern = dc.kern_stream;
+  const bool p2p = cfg.fanout == SLLM_FANOUT_P2P;
+  for (int s = 0; s < P.S; ++s) P.xfer[s] = p2p ? comm_stream(L->comm, s) : dc.streams[s];
+  P.kern = p2p ? comm_stream(L->comm, kMaxStreams) : dc.kern_stream;
   P.nslot = std::max(3, P.S + 1);
   // Chunks are the copy engine's transfer unit; kernels and copy submissions are
   // grouped per window of >= kWindowBytes so small chunks do not make the host issue
@@ -410,12 +442,19 @@ static void run_job(sllm_load* L, PartJob& j) {
   j.d_expect = reinterpret_cast<uint64_t*>(base + seg_bytes + acc_bytes);
   j.d_cs = reinterpret_cast<uint64_t*>(base + seg_bytes + acc_bytes + tab_bytes);
   j.d_bad = reinterpret_cast<unsigned long long*>(base + seg_bytes + acc_bytes + 2 * tab_bytes);
+  j.d_err = reinterpret_cast<uint32_t*>(j.d_bad + 1);
   SLLM_CUDA(cudaMemcpyAsync(j.d_segs, j.segs.data(), j.segs.size() * sizeof(Seg), cudaMemcpyHostToDevice, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_acc, 0, acc_bytes, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_cs, 0, tab_bytes, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_bad, 0xFF, 8, s0));
+  SLLM_CUDA(cudaMemsetAsync(j.d_err, 0, 4, s0));
   if (nb) SLLM_CUDA(cudaMemcpyAsync(j.d_expect, pr.checksums.data(), nb * 8, cudaMemcpyHostToDevice, s0));
   SLLM_CUDA(cudaEventRecord(j.ev[0], s0));
+  if (p2p) {  // no store into a peer replica before every peer is done verifying the previous load
+    const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
+    SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me) + R, R, me, j.epoch - 1, comm_timeout_ns(L->comm),
+                               j.d_err, s0));
+  }
   SLLM_CUDA(cudaEventRecord(j.ev[2], s0));
   for (int s = 1; s < P.S; ++s) SLLM_CUDA(cudaStreamWaitEvent(P.xfer[s], j.ev[2], 0));
   SLLM_CUDA(cudaStreamWaitEvent(P.kern, j.ev[2], 0));
@@ -457,25 +496,49 @@ static void run_job(sllm_load* L, PartJob& j) {
     }
     tails.push_back(cs);
     SLLM_CUDA(cudaEventDestroy(evk));
+  } else if (p2p) {
+    // Replicated load, fan-out fused into the loading kernels: this
+    // rank moves its slice [lo, hi) over PCIe and its kernels store it into every replica.
+    const uint64_t nch_hi = ceil_div(j.hi, C);
+    for (uint64_t k0 = j.lo / C, w = 0; k0 < nch_hi; k0 += P.window, ++w)
+      issue_window(idx, cfg, j, P, w, k0, std::min(k0 + P.window, nch_hi), k0 + P.window >= nch_hi);
+    join_streams(tails, s0);
+    tails.clear();
+    const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
+    // Signal array of rank q (2R words): ready[r] = last epoch whose stores rank r has
+    // completed into q's replica, done[r] = last epoch rank r has finished (its replica is
+    // free for the next epoch's stores).  Every store of this rank's kernels -> visible to
+    // the peers (ready), then wait for theirs, verify what arrived, publish done.
+    PeerSignal ready{}, done{};
+    for (int q = 0; q < R; ++q)
+      if (q != me) {
+        ready.remote[ready.n++] = comm_peer_signal(L->comm, q) + me;
+        done.remote[done.n++] = comm_peer_signal(L->comm, q) + R + me;
+      }
+    SLLM_CUDA(launch_peer_signal(ready, j.epoch, s0));
+    SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me), R, me, j.epoch, comm_timeout_ns(L->comm), j.d_err, s0));
+    j.fanout = pr.length - (j.hi - j.lo);
+    if (cfg.verify && idx.block) {  // what arrived over NVLink is verified like what came over PCIe
+      if (j.lo > 0) verify_range(idx, cfg, j, 0, j.lo, s0);
+      if (j.hi < pr.length) verify_range(idx, cfg, j, j.hi, pr.length, s0);
+    }
+    SLLM_CUDA(launch_peer_signal(done, j.epoch, s0));
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
     for (uint64_t k0 = 0, w = 0; k0 < nch; k0 += P.window, ++w)
       issue_window(idx, cfg, j, P, w, k0, std::min(k0 + P.window, nch), k0 + P.window >= nch);
   }
   // join every stream into s0, then let the caller's stream wait for the load
-  for (cudaStream_t t : tails) {
-    cudaEvent_t e;
-    SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    SLLM_CUDA(cudaEventRecord(e, t));
-    SLLM_CUDA(cudaStreamWaitEvent(s0, e, 0));
-    SLLM_CUDA(cudaEventDestroy(e));  // destruction is deferred until the event completes
-  }
+  join_streams(tails, s0);
   SLLM_CUDA(cudaEventRecord(j.ev[1], s0));
   if (j.origin) gate_open_device(s0, j.gate);  // releases the caller's stream on the device
   j.t_issue_ns = now_ns() - t0;
   SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
   j.fsrc.reset();  // file tier: readers are done, slots go back to the pinned pool
-  SLLM_CUDA(cudaMemcpy(&j.h_bad, j.d_bad, 8, cudaMemcpyDeviceToHost));
+  uint64_t tail[2] = {};
+  SLLM_CUDA(cudaMemcpy(tail, j.d_bad, 16, cudaMemcpyDeviceToHost));  // first failing block, peer-wait result
+  j.h_bad = tail[0];
+  j.h_err = (uint32_t)tail[1];
   SLLM_CUDA(cudaEventElapsedTime(&j.t_dev_ms, j.ev[0], j.ev[1]));
   for (auto* v : {&j.kev, &j.cev}) {
     double sum = 0;
@@ -492,6 +555,8 @@ static void run_job(sllm_load* L, PartJob& j) {
   cudaEventDestroy(P.copied);
   for (auto& e : P.freed) cudaEventDestroy(e);
   SLLM_CUDA(cudaGetLastError());
+  if (j.h_err) fail(SLLM_E_PEER, "P2P fan-out: peer rank " + std::to_string(j.h_err - 1) +
+                                     " did not signal completion within the timeout");
 }
 
 static void run_job_guarded(sllm_load* L, PartJob& j) {
@@ -530,8 +595,13 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (idx->block && cfg.chunk_bytes % idx->block) fail(SLLM_E_INVALID, "chunk size must be a multiple of the block size");
   if (cfg.chunk_bytes % idx->align) fail(SLLM_E_INVALID, "chunk size must be a multiple of the alignment");
   const bool scatter = cfg.mode == SLLM_MODE_SCATTER_CE || cfg.mode == SLLM_MODE_SCATTER_ZC;
-  if (cfg.fanout == SLLM_FANOUT_BCAST) {
+  if (cfg.fanout == SLLM_FANOUT_BCAST || cfg.fanout == SLLM_FANOUT_P2P) {
     if (!comm) fail(SLLM_E_INVALID, "fan-out needs a communicator");
+    if (cfg.fanout == SLLM_FANOUT_BCAST && comm_is_peers(comm))
+      fail(SLLM_E_INVALID, "SLLM_FANOUT_BCAST needs an NCCL communicator (sllm_comm_init_rank/_all)");
+    if (cfg.fanout == SLLM_FANOUT_P2P && !comm_is_peers(comm))
+      fail(SLLM_E_INVALID, "SLLM_FANOUT_P2P needs a peer group (sllm_comm_init_peers)");
+    if (cfg.fanout == SLLM_FANOUT_P2P && cfg.engine == 2) fail(SLLM_E_INVALID, "the P2P fan-out needs the TMA engine");
     if (idx->parts.size() != 1) fail(SLLM_E_INVALID, "fan-out needs a single-partition (replicated) index");
     if (scatter) fail(SLLM_E_INVALID, "fan-out supports the contiguous modes only");
   } else if (cfg.fanout != SLLM_FANOUT_NONE) {
@@ -562,8 +632,23 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
     j.dst_base = dst_base ? static_cast<uint8_t*>(dst_base[p]) : nullptr;
     j.origin = stream ? static_cast<cudaStream_t>(stream[p]) : nullptr;
     if (!scatter && !j.dst_base) fail(SLLM_E_INVALID, "null dst_base for a loaded partition");
-    if (cfg.fanout == SLLM_FANOUT_BCAST && comm_device(comm) != j.gpu)
+    if (cfg.fanout != SLLM_FANOUT_NONE && comm_device(comm) != j.gpu)
       fail(SLLM_E_INVALID, "communicator belongs to another GPU");
+    j.lo = 0;
+    j.hi = idx->parts[p].length;
+    if (cfg.fanout != SLLM_FANOUT_NONE) {  // this rank's slice: the only bytes it reads from the host
+      const int R = comm_nranks(comm), me = comm_rank(comm);
+      std::vector<uint64_t> lohi(2 * R);
+      if (sllm_replica_slices(j.hi, cfg.chunk_bytes, R, lohi.data()) != SLLM_OK) fail(SLLM_E_INVALID, "bad slices");
+      j.lo = lohi[2 * me];
+      j.hi = lohi[2 * me + 1];
+    }
+    if (cfg.fanout == SLLM_FANOUT_P2P) {
+      if (j.dst_base != comm_peer_base(comm, comm_rank(comm)))
+        fail(SLLM_E_INVALID, "P2P fan-out: dst_base must be this rank's replica of the peer group");
+      for (int q = 0; q < comm_nranks(comm); ++q)
+        if (q != comm_rank(comm)) j.peers[j.n_peers++] = comm_peer_base(comm, q);
+    }
     if (j.dst_base && (reinterpret_cast<uintptr_t>(j.dst_base) & 15)) fail(SLLM_E_INVALID, "dst_base must be 16-byte aligned");
     if (scatter) {
       for (uint32_t ti : idx->parts[p].by_offset) {
@@ -575,12 +660,14 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
     SLLM_CUDA(cudaSetDevice(j.gpu));
     if (!dir) {
       // the source must be page-locked host memory ("pinned memory ... DMA")
+      // (with a fan-out only the rank's slice needs to be pinned: check where it starts)
+      const uint64_t probe = j.hi > j.lo ? j.lo : 0;
       cudaPointerAttributes at{};
-      if (cudaPointerGetAttributes(&at, j.src) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+      if (cudaPointerGetAttributes(&at, j.src + probe) != cudaSuccess || at.type != cudaMemoryTypeHost) {
         cudaGetLastError();
         fail(SLLM_E_INVALID, "partition source is not pinned host memory (use sllm_host_alloc / sllm_host_register)");
       }
-      j.src_dev = static_cast<const uint8_t*>(at.devicePointer);
+      j.src_dev = at.devicePointer ? static_cast<const uint8_t*>(at.devicePointer) - probe : nullptr;
       if ((cfg.mode == SLLM_MODE_ZEROCOPY || cfg.mode == SLLM_MODE_SCATTER_ZC) && !j.src_dev)
         fail(SLLM_E_INVALID, "zero-copy modes need host memory mapped into the device address space");
     }
@@ -624,6 +711,8 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
     }
     throw;
   }
+  if (cfg.fanout == SLLM_FANOUT_P2P)  // one epoch per collective load, taken in call order
+    for (auto& j : L->jobs) j.epoch = comm_next_epoch(comm);
   for (auto& j : L->jobs) j.th = std::thread(run_job_guarded, L.get(), std::ref(j));
   return L.release();
 }

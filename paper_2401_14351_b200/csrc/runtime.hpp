@@ -69,5 +69,11 @@ void nccl_bcast_group(sllm_comm* comm, const std::vector<std::pair<uint64_t, uin
 int comm_nranks(const sllm_comm* c);
 int comm_rank(const sllm_comm* c);
 int comm_device(const sllm_comm* c);
+bool comm_is_peers(const sllm_comm* c);
+uint8_t* comm_peer_base(const sllm_comm* c, int q);
+uint32_t* comm_peer_signal(const sllm_comm* c, int q);
+uint64_t comm_timeout_ns(const sllm_comm* c);
+uint32_t comm_next_epoch(sllm_comm* c);
+cudaStream_t comm_stream(sllm_comm* c, int s);
 
 }  // namespace sllm

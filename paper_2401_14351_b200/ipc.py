@@ -68,3 +68,24 @@ class Imported:
 
 def import_tensors(exported: dict) -> Imported:
     return Imported(exported)
+
+
+def export_region(ptr: int, nbytes: int) -> bytes:
+    """sllm_ipc_export of one device range (e.g. a P2P replica or signal array)."""
+    r = _abi.IpcRegion()
+    check(lib().sllm_ipc_export(C.c_void_p(ptr), nbytes, C.byref(r)))
+    return bytes(r)
+
+
+def open_region(blob: bytes, gpu: int) -> int:
+    """Map an exported range into this process, in the context of CUDA device ``gpu`` (the
+    importing GPU: a peer's memory is then reached over NVLink)."""
+    r = _abi.IpcRegion.from_buffer_copy(blob)
+    r.gpu = gpu
+    out = C.c_void_p()
+    check(lib().sllm_ipc_open(C.byref(r), C.byref(out)))
+    return out.value
+
+
+def close(ptr: int) -> None:
+    check(lib().sllm_ipc_close(C.c_void_p(ptr)))
