@@ -141,6 +141,8 @@ SLLM_API sllm_status sllm_index_open(const char* path, sllm_index** out);
 SLLM_API sllm_status sllm_index_from_memory(const void* blob, size_t len, sllm_index** out);
 SLLM_API void sllm_index_close(sllm_index* index);
 SLLM_API sllm_status sllm_index_get_info(const sllm_index* index, sllm_index_info* out);
+/* SURVEY §8(b) sllm_index_counts: number of tensors and of partitions (either out may be NULL). */
+SLLM_API sllm_status sllm_index_counts(const sllm_index* index, size_t* n_tensors, size_t* n_partitions);
 /* Partition p (0..n_partitions-1, ascending device id). */
 SLLM_API sllm_status sllm_index_partition(const sllm_index* index, size_t p, int32_t* device_id,
                                  uint64_t* length, uint64_t* n_blocks, uint64_t* n_tensors);

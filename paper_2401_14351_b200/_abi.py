@@ -83,6 +83,7 @@ SIGNATURES = {
     "sllm_index_from_memory": (S, [P, C.c_size_t, PP]),
     "sllm_index_close": (None, [P]),
     "sllm_index_get_info": (S, [P, C.POINTER(IndexInfo)]),
+    "sllm_index_counts": (S, [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "sllm_index_partition": (S, [P, C.c_size_t, C.POINTER(C.c_int32), C.POINTER(U64), C.POINTER(U64), C.POINTER(U64)]),
     "sllm_index_block_checksums": (S, [P, C.c_size_t, C.POINTER(C.POINTER(U64))]),
     "sllm_index_tensor": (S, [P, C.c_size_t, C.POINTER(TensorInfo)]),

@@ -135,6 +135,12 @@ class Index:
         return buf.raw[:n.value]
 
     # -- queries -----------------------------------------------------------------------
+    def counts(self) -> Tuple[int, int]:
+        """(n_tensors, n_partitions) -- sllm_index_counts."""
+        nt, npart = C.c_size_t(), C.c_size_t()
+        check(lib().sllm_index_counts(self.handle, C.byref(nt), C.byref(npart)))
+        return nt.value, npart.value
+
     def info(self) -> dict:
         i = _abi.IndexInfo()
         check(lib().sllm_index_get_info(self._h, C.byref(i)))

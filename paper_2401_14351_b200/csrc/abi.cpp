@@ -117,6 +117,14 @@ sllm_status sllm_index_from_memory(const void* blob, size_t len, sllm_index** ou
 
 void sllm_index_close(sllm_index* idx) { delete idx; }
 
+sllm_status sllm_index_counts(const sllm_index* idx, size_t* n_tensors, size_t* n_partitions) {
+  return guard([&] {
+    if (!idx) fail(SLLM_E_INVALID, "null index");
+    if (n_tensors) *n_tensors = idx->tensors.size();
+    if (n_partitions) *n_partitions = idx->parts.size();
+  });
+}
+
 sllm_status sllm_index_get_info(const sllm_index* idx, sllm_index_info* out) {
   return guard([&] {
     if (!idx || !out) fail(SLLM_E_INVALID, "null argument");

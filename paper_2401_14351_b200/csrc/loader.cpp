@@ -454,6 +454,7 @@ static void run_job(sllm_load* L, PartJob& j) {
     const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
     SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me) + R, R, me, j.epoch - 1, comm_timeout_ns(L->comm),
                                j.d_err, s0));
+    if (R > 1) j.launches++;
   }
   SLLM_CUDA(cudaEventRecord(j.ev[2], s0));
   for (int s = 1; s < P.S; ++s) SLLM_CUDA(cudaStreamWaitEvent(P.xfer[s], j.ev[2], 0));
@@ -523,6 +524,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       if (j.hi < pr.length) verify_range(idx, cfg, j, j.hi, pr.length, s0);
     }
     SLLM_CUDA(launch_peer_signal(done, j.epoch, s0));
+    if (R > 1) j.launches += 3;  // ready signal, ready wait, done signal
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
     for (uint64_t k0 = 0, w = 0; k0 < nch; k0 += P.window, ++w)

@@ -75,6 +75,7 @@ def test_native_parses_oracle_index_and_back():
         assert idx.serialize() == blob
         info = idx.info()
         assert info["model_id"] == f"model-{seed}" and info["payload_bytes"] == lay.payload_bytes
+        assert idx.counts() == (len(lay.entries), len(lay.devices()))
         for t, e in zip(idx.tensors, lay.entries):
             assert (t.name, t.device, t.dtype, t.shape, t.offset, t.nbytes) == \
                 (e.name, e.device, e.dtype, e.shape, e.offset, e.size)
