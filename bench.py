@@ -421,10 +421,11 @@ def main():
         # Launches on the S streams overlap, so the kernel's rate is its bytes per step
         # over the step's device time (the kernel is the only work in the step).
         achieved = kern_bytes / (ms_step * 1e-3) / 1e9
-        traffic, traffic_src = ncu_traffic(args.mode, kern_bytes / kern_launches)
         roof = {"bound": "pcie", "achieved": achieved, "peak": b_h2d / world, "unit": "GB/s",
-                "frac": achieved / (b_h2d / world), "traffic": traffic, "traffic_source": traffic_src,
-                "traffic_note": "DRAM bytes (the HBM writes; the reads cross PCIe) per launch",
+                "frac": achieved / (b_h2d / world), "traffic": None,
+                "traffic_note": "the kernel's reads cross PCIe, not DRAM; its HBM writes mostly stay in the 126 MB "
+                                "L2 past the launch (profiles/r01/ncu_traffic_zerocopy.json: 12.9 MB of a 67.1 MB "
+                                "window reach DRAM within the launch), so ncu DRAM bytes do not measure it",
                 "kernel": "materialise_tma_kernel<store,check> (zero-copy host source)",
                 "launches_per_step": kern_launches, "avg_launch_ms": kern_ms / max(kern_launches, 1),
                 "peak_source": "cudaMemcpyAsync H2D from the same pinned buffer, 4 GiB, best of 5, this run"}
