@@ -59,6 +59,28 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+# SLLM_BENCH_SAME_GPU=1: every rank on cuda:0 with a gloo group -- a plumbing check of the
+# multi-rank paths (barriers, max-over-ranks timing, IPC peer groups) on a 1-GPU box; its
+# numbers share one PCIe link and are not scaling results.
+SAME_GPU = os.environ.get("SLLM_BENCH_SAME_GPU") == "1"
+
+
+def gpu_of(local):
+    return 0 if SAME_GPU else local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    """Max of a per-rank float over the job (device tensor on NCCL, host tensor on gloo)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    nccl = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=torch.cuda.current_device() if nccl else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -206,11 +228,7 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1):
                 dst[o:o + piece].copy_(src[o:o + piece], non_blocking=True)
             e.record()
             e.synchronize()
-            ms = s.elapsed_time(e)
-            if world > 1:
-                t = torch.tensor([ms], device=dst.device)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms = float(t.item())
+            ms = max_over_ranks(s.elapsed_time(e), world)
             best = max(best, world * n / (ms * 1e-3) / 1e9)
         out[name] = best
     return max(out.values()), out
@@ -265,8 +283,11 @@ def main():
     if world > 1:
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(gpu_of(local))
+        if SAME_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.impl == "reference":
         run_reference(args, rank, world)
         if world > 1:
@@ -281,8 +302,8 @@ def main():
     from synth import models, payload
 
     payload.build_csynth()
-    torch.cuda.set_device(local)
-    gpu = local
+    gpu = gpu_of(local)
+    torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
 
     # ---- setup (untimed): synthetic checkpoint packed into pinned DRAM by the converter
@@ -350,11 +371,7 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms_total = start.elapsed_time(end)
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = max_over_ranks(start.elapsed_time(end), world)
     ms_step = ms_total / args.steps
     # every rank ends the step with its own loaded model (sharded: its partition; replicated:
     # a full replica, of which it moved 1/N over PCIe)
@@ -377,11 +394,7 @@ def main():
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t0)
         del res, ix
-    t_e2e = min(e2e_t)
-    if world > 1:  # the job's end-to-end time is its slowest rank's
-        t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_e2e = float(t.item())
+    t_e2e = max_over_ranks(min(e2e_t), world)  # the job's end-to-end time is its slowest rank's
     e2e = {"value": payload_bytes * world / t_e2e / 1e9, "unit": "GB/s",
            "h2d_bytes_per_step": int(pcie_bytes) + sum(idx.partitions[p].n_blocks * 8 for p in parts),
            "d2h_bytes_per_step": 8 * len(parts),
@@ -452,7 +465,9 @@ def main():
                 "config": {"workload": args.config, "mode": args.mode, "fanout": args.fanout, "chunk_mib": args.chunk_mib,
                            "streams": args.streams, "ctas": args.ctas, "payload_bytes_per_gpu": payload_bytes,
                            "raw_bytes_per_gpu": raw_bytes, "verify": "fletcher64 per 1 MiB block, every block",
-                           "l2": "inputs 13 GB >> 126 MB L2, no flush needed", "parallelism": f"replicated x{world} ({args.fanout})" if replicated else f"sharded x{world}"},
+                           "l2": "inputs 13 GB >> 126 MB L2, no flush needed", "parallelism": f"replicated x{world} ({args.fanout})" if replicated else f"sharded x{world}",
+                           **({"same_gpu_plumbing_check": "all ranks on cuda:0 (gloo); not a scaling number"}
+                              if SAME_GPU and world > 1 else {})},
                 "time_to_loaded_model_s": ms_step * 1e-3, "t_alloc_s": t_alloc, "t_setup_s": t_setup,
                 "b_h2d_measured_GBps": b_h2d, "frac_h2d": pcie_rate / b_h2d,
                 "gpu_launches": int(rep["kernel_launches"]) * args.steps,
