@@ -108,6 +108,7 @@ struct PartJob {
   uint64_t kernel_bytes = 0;
   double kernel_ms = 0, copy_ms = 0;
   std::thread th;
+  std::vector<cudaStream_t> used;  // streams this job queued work on (drained on failure)
 };
 
 }  // namespace sllm
@@ -424,6 +425,9 @@ static void run_job(sllm_load* L, PartJob& j) {
     for (auto& e : P.freed) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t s0 = P.xfer[0];
+  j.used.assign(P.xfer, P.xfer + P.S);
+  j.used.push_back(P.kern);
+  if (cfg.fanout == SLLM_FANOUT_BCAST) j.used.push_back(dc.comm_stream);
   const uint64_t nb = pr.n_blocks;
   const size_t seg_bytes = align_up(j.segs.size() * sizeof(Seg), 256);
   const size_t acc_bytes = align_up(std::max<uint64_t>(nb, 1) * sizeof(BlockAcc), 256);
@@ -570,6 +574,13 @@ static void run_job_guarded(sllm_load* L, PartJob& j) {
   } catch (const std::exception& e) {
     j.status = SLLM_E_INVALID;
     j.error = e.what();
+  }
+  if (j.status != SLLM_OK && j.gpu >= 0) {
+    // a failure part-way through issuing: let what was queued finish before the scratch,
+    // staging and events it uses can be released by sllm_load_free
+    cudaSetDevice(j.gpu);
+    for (cudaStream_t st : j.used) cudaStreamSynchronize(st);
+    cudaGetLastError();
   }
   gate_open_host(j.gate);  // never leave the caller's stream waiting (success or failure)
 }
