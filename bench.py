@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--chunk-mib", type=int, default=64)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--all-partitions", action="store_true",
+                    help="load every partition of a multi-partition config onto this rank's GPU (e.g. the whole "
+                         "LLaMA-2-70B TP8 checkpoint on one B200)")
     ap.add_argument("--fanout", default="none", choices=["none", "bcast", "p2p"],
                     help="replicated checkpoint: every rank ends with a full replica; rank r reads slice r over "
                          "PCIe and the rest arrives over NVLink (bcast: NCCL broadcasts, p2p: fused peer stores)")
@@ -312,8 +315,13 @@ def main():
     replicated = args.fanout != "none"
     if replicated and len(set(t.device for t in inv)) != 1:
         raise SystemExit("--fanout needs a single-partition (replicated) checkpoint config")
-    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=[0] if world == 1 or
-                                       len(set(t.device for t in inv)) == 1 else [rank], gpu_of={0: gpu, rank: gpu})
+    n_parts = len(set(t.device for t in inv))
+    if args.all_partitions:
+        sel = list(range(n_parts))
+    else:
+        sel = [0] if world == 1 or n_parts == 1 else [rank]
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=sel,
+                                       gpu_of={p: gpu for p in sel})
     t_setup = time.perf_counter() - t0
     blob = idx.serialize()
     parts = sorted(bufs)
@@ -463,9 +471,10 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic",
                 "config": {"workload": args.config, "mode": args.mode, "fanout": args.fanout, "chunk_mib": args.chunk_mib,
-                           "streams": args.streams, "ctas": args.ctas, "payload_bytes_per_gpu": payload_bytes,
+                           "streams": args.streams, "ctas": args.ctas, "partitions_per_gpu": len(parts),
+                           "payload_bytes_per_gpu": payload_bytes,
                            "raw_bytes_per_gpu": raw_bytes, "verify": "fletcher64 per 1 MiB block, every block",
-                           "l2": "inputs 13 GB >> 126 MB L2, no flush needed", "parallelism": f"replicated x{world} ({args.fanout})" if replicated else f"sharded x{world}",
+                           "l2": f"inputs {raw_bytes / 1e9:.1f} GB per GPU >> 126 MB L2, no flush needed", "parallelism": f"replicated x{world} ({args.fanout})" if replicated else f"sharded x{world}",
                            **({"same_gpu_plumbing_check": "all ranks on cuda:0 (gloo); not a scaling number"}
                               if SAME_GPU and world > 1 else {})},
                 "time_to_loaded_model_s": ms_step * 1e-3, "t_alloc_s": t_alloc, "t_setup_s": t_setup,
