@@ -197,41 +197,48 @@ void seal(sllm_index* idx, const void* const* part_bufs) {
   idx->sealed = true;
 }
 
-// Copy every tensor's payload to its slot, zero every other byte (Q3), then seal.
+// Copy every tensor's payload to its slot, zero every other byte (Q3) and compute the
+// block checksums -- fused per checksum block: a worker fills block j (tensor pieces and
+// padding, in offset order) and checksums it while it is still in its core's cache, so
+// the partition bytes are written once and never re-read from DRAM (a separate seal pass
+// would read all of them again).
 void convert_into(const sllm_src_tensor* t, size_t n, sllm_index* idx, void* const* part_bufs) {
   if (n != idx->tensors.size()) fail(SLLM_E_INVALID, "tensor count differs from the plan");
   if (!part_bufs && !idx->parts.empty()) fail(SLLM_E_INVALID, "null partition buffer array");
   for (size_t p = 0; p < idx->parts.size(); ++p)
     if (!part_bufs[p]) fail(SLLM_E_INVALID, "null partition buffer");
-  struct Job { uint8_t* dst; const uint8_t* src; uint64_t len; };  // src == nullptr: zero fill
-  std::vector<Job> jobs;
-  const uint64_t kPiece = 64ull << 20;
-  auto add = [&](uint8_t* dst, const uint8_t* src, uint64_t len) {
-    for (uint64_t o = 0; o < len; o += kPiece)
-      jobs.push_back({dst + o, src ? src + o : nullptr, std::min(kPiece, len - o)});
-  };
   for (size_t i = 0; i < n; ++i) {
     const TensorRec& r = idx->tensors[i];
     if (std::strcmp(t[i].name ? t[i].name : "", r.name.c_str()) || t[i].nbytes != r.nbytes)
       fail(SLLM_E_CONVERSION, "tensor " + std::to_string(i) + " differs from the plan");
     if (!t[i].data) fail(SLLM_E_INVALID, "null data for '" + r.name + "'");
-    add(static_cast<uint8_t*>(part_bufs[r.part]) + r.offset, static_cast<const uint8_t*>(t[i].data), r.nbytes);
   }
-  for (size_t p = 0; p < idx->parts.size(); ++p) {
-    uint8_t* base = static_cast<uint8_t*>(part_bufs[p]);
-    uint64_t cur = 0;
-    for (uint32_t ti : idx->parts[p].by_offset) {
-      const TensorRec& r = idx->tensors[ti];
-      if (r.offset > cur) add(base + cur, nullptr, r.offset - cur);
-      cur = r.offset + r.nbytes;
-    }
-    if (idx->parts[p].length > cur) add(base + cur, nullptr, idx->parts[p].length - cur);
-  }
+  const uint64_t B = idx->block ? idx->block : (4ull << 20);  // work unit: one checksum block
+  struct Job { size_t p; uint64_t j; };
+  std::vector<Job> jobs;
+  for (size_t p = 0; p < idx->parts.size(); ++p)
+    for (uint64_t j = 0; j < ceil_div(idx->parts[p].length, B); ++j) jobs.push_back({p, j});
   parallel_for(jobs.size(), default_threads(), [&](size_t i) {
-    if (jobs[i].src) std::memcpy(jobs[i].dst, jobs[i].src, jobs[i].len);
-    else std::memset(jobs[i].dst, 0, jobs[i].len);
+    PartRec& pr = idx->parts[jobs[i].p];
+    uint8_t* base = static_cast<uint8_t*>(part_bufs[jobs[i].p]);
+    const uint64_t lo = jobs[i].j * B, hi = std::min(lo + B, pr.length);
+    // first tensor (in offset order) that ends after lo
+    auto it = std::partition_point(pr.by_offset.begin(), pr.by_offset.end(), [&](uint32_t ti) {
+      return idx->tensors[ti].offset + idx->tensors[ti].nbytes <= lo;
+    });
+    uint64_t cur = lo;
+    for (; it != pr.by_offset.end(); ++it) {
+      const TensorRec& r = idx->tensors[*it];
+      if (r.offset >= hi) break;
+      const uint64_t a = std::max(r.offset, lo), b = std::min(r.offset + r.nbytes, hi);
+      if (a > cur) std::memset(base + cur, 0, a - cur);
+      std::memcpy(base + a, static_cast<const uint8_t*>(t[*it].data) + (a - r.offset), b - a);
+      cur = b;
+    }
+    if (hi > cur) std::memset(base + cur, 0, hi - cur);
+    if (idx->block) pr.checksums[jobs[i].j] = fletcher64(base + lo, hi - lo);
   });
-  seal(idx, part_bufs);
+  idx->sealed = true;
 }
 
 // ---------------------------------------------------------------------------------
