@@ -388,6 +388,9 @@ def main():
 
     # ---- end-to-end through the public API (a2 allocation + index open + load + wait +
     #      D2H of the verification word), host wall clock, pinned sources
+    if comm is None:  # e2e allocates its own destinations: give the timed loop's back first
+        bases = per_tensor = None
+        torch.cuda.empty_cache()
     e2e_t = []
     for _ in range(2):
         torch.cuda.synchronize()
@@ -452,7 +455,7 @@ def main():
                 "peak_source": "cudaMemcpyAsync H2D from the same pinned buffer, 4 GiB, best of 5, this run"}
     standalone = None
     if not args.no_standalone and rank == 0:
-        del bases, per_tensor
+        bases = per_tensor = None
         torch.cuda.empty_cache()
         standalone = standalone_hbm(idx, torch, sllm)
         hbm = peaks().get("hbm_gbs", 6551.4)
