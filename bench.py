@@ -137,7 +137,7 @@ def peaks():
         return {}
 
 
-def ncu_traffic(mode, bytes_per_launch):
+def ncu_traffic(mode, bytes_per_launch, key="traffic_over_algorithmic"):
     """`traffic` for the roofline: DRAM bytes per launch from the committed `ncu --set full`
     capture of an in-pipeline launch (profiles/<round>/ncu_traffic_<mode>.json, written by
     tools/ncu_traffic.py), scaled from the captured launch's algorithmic bytes to this
@@ -147,7 +147,9 @@ def ncu_traffic(mode, bytes_per_launch):
     if not hits:
         return None, None
     cap = json.load(open(hits[-1]))
-    return cap["traffic_over_algorithmic"] * bytes_per_launch, os.path.relpath(hits[-1], ROOT)
+    if key not in cap:
+        return None, None
+    return cap[key] * bytes_per_launch, os.path.relpath(hits[-1], ROOT)
 
 
 def run_reference(args, rank, world):
@@ -445,11 +447,11 @@ def main():
         # Launches on the S streams overlap, so the kernel's rate is its bytes per step
         # over the step's device time (the kernel is the only work in the step).
         achieved = kern_bytes / (ms_step * 1e-3) / 1e9
+        traffic, traffic_src = ncu_traffic(args.mode, kern_bytes / kern_launches, key="sysmem_over_algorithmic")
         roof = {"bound": "pcie", "achieved": achieved, "peak": b_h2d / world, "unit": "GB/s",
-                "frac": achieved / (b_h2d / world), "traffic": None,
-                "traffic_note": "the kernel's reads cross PCIe, not DRAM; its HBM writes mostly stay in the 126 MB "
-                                "L2 past the launch (profiles/r01/ncu_traffic_zerocopy.json: 12.9 MB of a 67.1 MB "
-                                "window reach DRAM within the launch), so ncu DRAM bytes do not measure it",
+                "frac": achieved / (b_h2d / world), "traffic": traffic, "traffic_source": traffic_src,
+                "traffic_note": "bytes the launch pulled from host memory over PCIe (ncu syslts sysmem sectors x 32) "
+                                "-- the bounding link; its HBM writes mostly stay in the 126 MB L2 past the launch",
                 "kernel": "materialise_tma_kernel<store,check> (zero-copy host source)",
                 "launches_per_step": kern_launches, "avg_launch_ms": kern_ms / max(kern_launches, 1),
                 "peak_source": "cudaMemcpyAsync H2D from the same pinned buffer, 4 GiB, best of 5, this run"}

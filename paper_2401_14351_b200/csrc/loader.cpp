@@ -416,8 +416,14 @@ static void run_job(sllm_load* L, PartJob& j) {
   // Chunks are the copy engine's transfer unit; kernels and copy submissions are
   // grouped per window of >= kWindowBytes so small chunks do not make the host issue
   // loop (one API call per chunk) the bottleneck.
-  P.window = cfg.fanout == SLLM_FANOUT_BCAST ? 1 : std::max<uint64_t>(1, kWindowBytes / cfg.chunk_bytes);
-  P.slot_bytes = P.window * cfg.chunk_bytes;
+  // SCATTER_CE stages whole windows in HBM and scatters each with one K3 launch: larger
+  // windows there (kScatterWindowBytes) make fewer, longer launches; the staging ring is
+  // never larger than the partition.
+  const uint64_t win_bytes = cfg.mode == SLLM_MODE_SCATTER_CE ? kScatterWindowBytes : kWindowBytes;
+  P.window = cfg.fanout == SLLM_FANOUT_BCAST ? 1 : std::max<uint64_t>(1, win_bytes / cfg.chunk_bytes);
+  const uint64_t nch_all = std::max<uint64_t>(1, ceil_div(pr.length, cfg.chunk_bytes));
+  P.slot_bytes = std::min(P.window, nch_all) * cfg.chunk_bytes;
+  P.nslot = (int)std::min<uint64_t>((uint64_t)P.nslot, ceil_div(nch_all, P.window));
   if (!j.file.empty()) j.fsrc = file_source_open(j.file, pr.length, P.window * cfg.chunk_bytes, j.io_threads, j.gpu);
   SLLM_CUDA(cudaEventCreateWithFlags(&P.copied, cudaEventDisableTiming));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {

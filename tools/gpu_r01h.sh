@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python tools/bench_convert.py --config opt-6.7b > gpurun_out/bench_convert.jsonl 2>&1
 timeout 1200 python bench.py --config llama2-70b-tp8 --all-partitions --steps 3 --warmup 3 --no-standalone --cpu-sample-gib 2 > gpurun_out/bench_70b_tp8_all.json 2> gpurun_out/bench_70b_tp8_all.err

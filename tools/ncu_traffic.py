@@ -21,7 +21,8 @@ import sys
 
 METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,launch__grid_size,"
-           "sm__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum")
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,"
+           "syslts__t_sectors_aperture_sysmem_lookup_miss.sum")
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1, "nsecond": 1e-9}
 
@@ -37,7 +38,7 @@ def main():
         d = {}
         for h, u, v in zip(head, units, r):
             if h in METRICS.split(","):
-                d[h] = float(v.replace(",", "")) * SCALE.get(u, 1)
+                d[h] = float(v.replace(",", "")) * (SCALE.get(u, 1) if u != "sector" else 1)
         d["kernel"] = r[head.index("Kernel Name")]
         launches.append(d)
     L = launches[0]
@@ -48,6 +49,9 @@ def main():
         "dram_bytes": traffic, "dram_read": L["dram__bytes_read.sum"], "dram_write": L["dram__bytes_write.sum"],
         "traffic_over_algorithmic": traffic / alg, "duration_s": L["gpu__time_duration.sum"],
         "dram_pct_of_peak": L.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+        # host (sysmem) sectors the kernel pulled through the L2 -- the PCIe reads of a zero-copy launch
+        "sysmem_read_bytes": 32 * L.get("syslts__t_sectors_aperture_sysmem_lookup_miss.sum", 0.0),
+        "sysmem_over_algorithmic": 32 * L.get("syslts__t_sectors_aperture_sysmem_lookup_miss.sum", 0.0) / alg,
         "note": "ncu replays the launch with caches flushed (cold), serialised: the duration is not the "
                 "in-pipeline time; the byte counts are the kernel's DRAM traffic for that launch"}, indent=1))
 
