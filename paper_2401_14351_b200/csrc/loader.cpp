@@ -40,19 +40,33 @@ DeviceCtx& device_ctx(int dev) {
   return *g_ctx[dev];
 }
 
-void DeviceCtx::ensure(int n) {
-  if (!streams[0]) {  // keep stream-ordered allocations (scratch, staging) cached between loads
+StreamSet* DeviceCtx::acquire(int n) {
+  if (!misc) {  // first use: keep stream-ordered allocations (scratch, staging) cached between loads
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();
+    SLLM_CUDA(cudaStreamCreateWithFlags(&misc, cudaStreamNonBlocking));
+  }
+  StreamSet* ss = nullptr;
+  if (!idle.empty()) {
+    ss = idle.back();
+    idle.pop_back();
+  } else {
+    sets.emplace_back(new StreamSet);
+    ss = sets.back().get();
   }
   for (int s = 0; s < n; ++s)
-    if (!streams[s]) SLLM_CUDA(cudaStreamCreateWithFlags(&streams[s], cudaStreamNonBlocking));
-  if (!comm_stream) SLLM_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
-  if (!kern_stream) SLLM_CUDA(cudaStreamCreateWithFlags(&kern_stream, cudaStreamNonBlocking));
+    if (!ss->xfer[s]) SLLM_CUDA(cudaStreamCreateWithFlags(&ss->xfer[s], cudaStreamNonBlocking));
+  if (!ss->kern) SLLM_CUDA(cudaStreamCreateWithFlags(&ss->kern, cudaStreamNonBlocking));
+  if (!ss->comm) SLLM_CUDA(cudaStreamCreateWithFlags(&ss->comm, cudaStreamNonBlocking));
+  return ss;
+}
+
+void DeviceCtx::release(StreamSet* s) {
+  if (s) idle.push_back(s);
 }
 
 // ------------------------------------------------------------------------------------
@@ -109,6 +123,7 @@ struct PartJob {
   double kernel_ms = 0, copy_ms = 0;
   std::thread th;
   std::vector<cudaStream_t> used;  // streams this job queued work on (drained on failure)
+  StreamSet* ss = nullptr;         // leased from the GPU's DeviceCtx for the job's lifetime
 };
 
 }  // namespace sllm
@@ -405,13 +420,13 @@ static void run_job(sllm_load* L, PartJob& j) {
   DeviceCtx& dc = device_ctx(j.gpu);
   {
     std::lock_guard<std::mutex> g(dc.mu);
-    dc.ensure(cfg.n_streams);
+    j.ss = dc.acquire(cfg.n_streams);
   }
   Pipe P;
   P.S = cfg.n_streams;
   const bool p2p = cfg.fanout == SLLM_FANOUT_P2P;
-  for (int s = 0; s < P.S; ++s) P.xfer[s] = p2p ? comm_stream(L->comm, s) : dc.streams[s];
-  P.kern = p2p ? comm_stream(L->comm, kMaxStreams) : dc.kern_stream;
+  for (int s = 0; s < P.S; ++s) P.xfer[s] = p2p ? comm_stream(L->comm, s) : j.ss->xfer[s];
+  P.kern = p2p ? comm_stream(L->comm, kMaxStreams) : j.ss->kern;
   P.nslot = std::max(3, P.S + 1);
   // Chunks are the copy engine's transfer unit; kernels and copy submissions are
   // grouped per window of >= kWindowBytes so small chunks do not make the host issue
@@ -433,7 +448,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   cudaStream_t s0 = P.xfer[0];
   j.used.assign(P.xfer, P.xfer + P.S);
   j.used.push_back(P.kern);
-  if (cfg.fanout == SLLM_FANOUT_BCAST) j.used.push_back(dc.comm_stream);
+  if (cfg.fanout == SLLM_FANOUT_BCAST) j.used.push_back(j.ss->comm);
   const uint64_t nb = pr.n_blocks;
   const size_t seg_bytes = align_up(j.segs.size() * sizeof(Seg), 256);
   const size_t acc_bytes = align_up(std::max<uint64_t>(nb, 1) * sizeof(BlockAcc), 256);
@@ -484,7 +499,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       fail(SLLM_E_INVALID, "fan-out schedule failed");
     cudaEvent_t evk;
     SLLM_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
-    cudaStream_t cs = dc.comm_stream;
+    cudaStream_t cs = j.ss->comm;
     SLLM_CUDA(cudaStreamWaitEvent(cs, j.ev[2], 0));
     for (uint64_t r = 0; r < rounds; ++r) {
       if (sllm_replica_round(pr.length, C, R, r, lohi.data(), nullptr) != SLLM_OK)
@@ -587,6 +602,12 @@ static void run_job_guarded(sllm_load* L, PartJob& j) {
     cudaSetDevice(j.gpu);
     for (cudaStream_t st : j.used) cudaStreamSynchronize(st);
     cudaGetLastError();
+  }
+  if (j.ss) {  // every stream of the set is idle now (synchronized above or in run_job)
+    DeviceCtx& dc = device_ctx(j.gpu);
+    std::lock_guard<std::mutex> g(dc.mu);
+    dc.release(j.ss);
+    j.ss = nullptr;
   }
   gate_open_host(j.gate);  // never leave the caller's stream waiting (success or failure)
 }
@@ -837,8 +858,9 @@ void sllm_load_free_internal(sllm_load* L) {
   join_load(L);
   for (auto& j : L->jobs) {
     if (j.gpu >= 0) cudaSetDevice(j.gpu);
-    if (j.scratch) cudaFreeAsync(j.scratch, device_ctx(j.gpu).streams[0]);
-    if (j.staging) cudaFreeAsync(j.staging, device_ctx(j.gpu).streams[0]);
+    DeviceCtx& dc = device_ctx(j.gpu);
+    if (j.scratch) cudaFreeAsync(j.scratch, dc.misc);
+    if (j.staging) cudaFreeAsync(j.staging, dc.misc);
     for (auto& e : j.ev)
       if (e) cudaEventDestroy(e);
     gate_release(j.gate);

@@ -26,13 +26,22 @@ constexpr uint64_t kVerifyBytes = 2048ull << 20;  // CE mode: max bytes per veri
 constexpr uint64_t kScatterWindowBytes = 256ull << 20;  // SCATTER_CE: bytes per staging slot / K3 launch
 
 // Library-owned, per-GPU resources reused across loads (no allocation in the hot path).
+// Every running partition job leases its own stream set, so concurrent jobs on one GPU
+// (several partitions, several loads) never queue behind each other's waits and their
+// per-launch timings stay their own.
+struct StreamSet {
+  cudaStream_t xfer[kMaxStreams] = {};
+  cudaStream_t kern = nullptr;
+  cudaStream_t comm = nullptr;
+};
 struct DeviceCtx {
   int dev = -1;
   std::mutex mu;
-  cudaStream_t streams[kMaxStreams] = {};
-  cudaStream_t comm_stream = nullptr;
-  cudaStream_t kern_stream = nullptr;
-  void ensure(int n_streams);                          // caller holds mu, device set
+  cudaStream_t misc = nullptr;                         // scratch frees after a load
+  std::vector<std::unique_ptr<StreamSet>> sets;
+  std::vector<StreamSet*> idle;
+  StreamSet* acquire(int n_streams);                   // caller holds mu, device set
+  void release(StreamSet* s);                          // caller holds mu
 };
 DeviceCtx& device_ctx(int dev);
 
