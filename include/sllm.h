@@ -219,7 +219,8 @@ typedef struct {
   int32_t verify;       /* 1 = check every block's Fletcher-64 against the index            */
   int32_t ctas;         /* CTAs per kernel launch (0 = mode default)                        */
   int32_t profile;      /* 1 = time every kernel launch with CUDA events, 2 = also copies    */
-  int32_t engine;       /* kernel engine: 0 = default (TMA), 1 = TMA bulk-copy ring, 2 = LDG tiles */
+  int32_t engine;       /* kernel engine: 0 = default (TMA), 1 = TMA bulk-load ring + vector stores,
+                           2 = LDG/STG register tiles, 3 = TMA bulk-load ring + TMA bulk stores */
   int32_t reserved;     /* must be 0                                                        */
 } sllm_load_config;
 

@@ -273,7 +273,7 @@ class LoadConfig:
     verify: bool = True
     ctas: int = 0
     profile: bool = False         # per-launch CUDA-event timing (bench roofline)
-    engine: str = "tma"           # tma (bulk-copy smem ring) | ldg (register tiles)
+    engine: str = "tma"           # tma (bulk-load smem ring) | tma_store (+ bulk stores) | ldg (register tiles)
 
     def to_c(self) -> _abi.LoadConfig:
         modes = {"ce": _abi.MODE_CE, "zerocopy": _abi.MODE_ZEROCOPY, "scatter_ce": _abi.MODE_SCATTER_CE,
@@ -281,7 +281,7 @@ class LoadConfig:
         fan = {"none": _abi.FANOUT_NONE, "bcast": _abi.FANOUT_BCAST, "p2p": _abi.FANOUT_P2P}
         return _abi.LoadConfig(self.chunk_bytes, self.n_streams, modes[self.mode], fan[self.fanout],
                                int(self.verify), self.ctas, int(self.profile),
-                               {"tma": 1, "ldg": 2}[self.engine], 0)
+                               {"tma": 1, "ldg": 2, "tma_store": 3}[self.engine], 0)
 
     @property
     def scatter(self) -> bool:

@@ -1,10 +1,23 @@
 // Device-resident entry points of the kernels (K4 checksum, K3 scatter) for partitions
 // already in HBM -- also how bench.py measures them standalone against the HBM roofline.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "runtime.hpp"
 
 namespace sllm {
+
+// Kernel engine of the standalone entry points: kDefaultEngine, or SLLM_STANDALONE_ENGINE
+// = ldg | tma | tma_store (a measurement knob for A/B runs of the same kernel family).
+static int standalone_engine() {
+  const char* e = getenv("SLLM_STANDALONE_ENGINE");
+  if (!e || !*e) return kDefaultEngine;
+  if (!strcmp(e, "ldg")) return 0;
+  if (!strcmp(e, "tma")) return 1;
+  if (!strcmp(e, "tma_store")) return 2;
+  fail(SLLM_E_INVALID, std::string("SLLM_STANDALONE_ENGINE: unknown engine '") + e + "'");
+}
 
 static int default_grid() {
   int dev = 0, sms = 148;
@@ -43,7 +56,7 @@ void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint6
   mp.acc = reinterpret_cast<BlockAcc*>(b);
   mp.cs_out = out;
   mp.bad = bad;
-  mp.engine = 1;
+  mp.engine = standalone_engine();
   SLLM_CUDA(launch_materialise(mp, MatKind::kChecksumOnly, ctas > 0 ? ctas : default_grid(), st));
   SLLM_CUDA(cudaFreeAsync(scratch, st));
 }
@@ -94,7 +107,7 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   mp.acc = d_acc;
   mp.expect = check ? d_expect : nullptr;
   mp.bad = d_bad;
-  mp.engine = 1;
+  mp.engine = standalone_engine();
   SLLM_CUDA(launch_materialise(mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas > 0 ? ctas : default_grid(), st));
   unsigned long long bad = ~0ull;
   SLLM_CUDA(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st));

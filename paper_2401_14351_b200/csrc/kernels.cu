@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(kThreads) materialise_kernel(const MatParams p
 // flight per SM covers HBM latency (K3/K4) and, with a few CTAs, PCIe latency (K2).
 // ---------------------------------------------------------------------------------
 constexpr int kConsumerWarps = 8;
-constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
+constexpr int kTmaThreads = 32 * (kConsumerWarps + 2);  // producer, 8 consumers, bulk storer
+constexpr int kStoreLag = 4;                             // bulk-store groups in flight per CTA
 constexpr uint32_t kStageBytes = 16u << 10;
 constexpr int kStages = 12;
 constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + 2 * kStages * sizeof(uint64_t);
@@ -215,6 +216,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
+// smem -> global bulk copy (TMA store, SASS UBLKCP), tracked by bulk async-groups.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(gdst), "r"(smem_addr(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {  // <= N most recent groups may still read smem
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ uint4 lds16(const uint8_t* p) {
   uint4 r;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -237,10 +249,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   const uint64_t unit = blk / p.split;
   const uint64_t u_first = p.lo / unit, u_end = (p.hi + unit - 1) / unit;
 
+  // engine 2: the tensor bytes leave shared memory by TMA bulk stores issued by one
+  // storer thread (contiguous pieces: segment x stage); consumers then only read smem for
+  // the checksum and write the < 16-byte tails of tensors.
+  const bool bulk_store = kStore && p.engine == 2 && p.n_peers == 0 && !p.no_seg_store;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kConsumerWarps);
+      mbar_init(&empty[i], kConsumerWarps + (bulk_store ? 1 : 0));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -260,6 +276,51 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
+    }
+    return;
+  }
+
+  if (warp == kConsumerWarps + 1) {  // bulk storer
+    if (bulk_store && lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      uint32_t ring[kStoreLag + 1];
+      int head = 0, cnt = 0;  // stages whose stores may still read smem, oldest first
+      for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x) {
+        const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
+        uint32_t lo = p.seg_begin, hi = p.seg_end;
+        while (hi - lo > 1) {
+          uint32_t mid = (lo + hi) >> 1;
+          if (p.segs[mid].off <= a) lo = mid; else hi = mid;
+        }
+        uint32_t cur = lo;
+        Seg sg = p.segs[cur];
+        for (uint64_t off = a; off < e; off += kStageBytes) {
+          const uint64_t end = off + min((uint64_t)kStageBytes, e - off);
+          mbar_wait(&full[stage], phase);
+          const uint8_t* sb = smem + (size_t)stage * kStageBytes;
+          while (off >= sg.off + sg.len && cur + 1 < p.seg_end) sg = p.segs[++cur];
+          uint32_t k = cur;
+          Seg s2 = sg;
+          for (;;) {  // every segment piece of this stage: one bulk store of its whole vectors
+            const uint64_t x0 = max(s2.off, off), x1 = min(min(s2.off + s2.len, end), (uint64_t)(s2.off + (s2.valid & ~(uint64_t)15)));
+            if (s2.dst && x1 > x0) bulk_s2g(s2.dst + (x0 - s2.off), sb + (x0 - off), (uint32_t)(x1 - x0));
+            if (s2.off + s2.len >= end || k + 1 >= p.seg_end) break;
+            s2 = p.segs[++k];
+          }
+          bulk_commit();
+          ring[(head + cnt) % (kStoreLag + 1)] = stage;
+          if (++cnt > kStoreLag) {
+            bulk_wait_read<kStoreLag>();
+            mbar_arrive(&empty[ring[head]]);
+            head = (head + 1) % (kStoreLag + 1);
+            --cnt;
+          }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+      bulk_wait_read<0>();
+      for (; cnt; --cnt, head = (head + 1) % (kStoreLag + 1)) mbar_arrive(&empty[ring[head]]);
+      bulk_wait_all();
     }
     return;
   }
@@ -295,8 +356,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           while (x >= sg.off + sg.len && cur + 1 < p.seg_end) sg = p.segs[++cur];
           if (sg.dst && !p.no_seg_store) {
             const uint64_t rel = x - sg.off;
-            if (rel + 16 <= sg.valid) store16(sg.dst + rel, val);
-            else if (rel < sg.valid) store_partial(sg.dst + rel, val, (uint32_t)(sg.valid - rel));
+            if (rel + 16 <= sg.valid) {
+              if (!bulk_store) store16(sg.dst + rel, val);
+            } else if (rel < sg.valid) {
+              store_partial(sg.dst + rel, val, (uint32_t)(sg.valid - rel));
+            }
           }
           // P2P fan-out: the same vector to every peer replica (NVLink stores; partitions are
           // multiples of the alignment >= 16, so whole vectors only)
@@ -474,7 +538,7 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
 cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream) {
   if (p.hi <= p.lo) return cudaSuccess;
   if (grid < 1) grid = num_sms();  // default: one CTA per SM
-  if (p.engine == 1) {
+  if (p.engine >= 1) {
     switch (kind) {
       case MatKind::kChecksumOnly: return launch_tma<false, true>(p, grid, stream);
       case MatKind::kCopyChecksum: return launch_tma<true, true>(p, grid, stream);

@@ -42,7 +42,8 @@ struct MatParams {
   uint64_t* cs_out;          // computed block checksums, or nullptr
   unsigned long long* bad;   // min failing block index (init UINT64_MAX)
   int host_src;              // 1: src is host-mapped pinned memory (zero-copy over PCIe)
-  int engine;                // 0: LDG/STG tiles; 1: TMA bulk copies through a shared-memory ring
+  int engine;                // 0: LDG/STG tiles; 1: TMA bulk loads through a shared-memory ring,
+                             // STG stores; 2: as 1 with TMA bulk stores out of the ring
   uint32_t split;            // TMA engine: units per checksum block (set by the launcher)
   // P2P fan-out (TMA engine, contiguous single segment): every stored vector of partition
   // offset x also goes to peer[k] + x -- device pointers to the other GPUs' replicas,

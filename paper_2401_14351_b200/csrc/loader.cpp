@@ -234,6 +234,17 @@ struct Pipe {
   uint64_t v_k0 = 0, v_k1 = 0;             // CE: landed chunks not yet verified [v_k0, v_k1)
 };
 
+// sllm_load_config.engine -> MatParams.engine (0 LDG tiles, 1 TMA ring + STG, 2 TMA ring +
+// TMA bulk stores).  Default: kDefaultEngine.
+static int kernel_engine(int cfg_engine) {
+  switch (cfg_engine) {
+    case 1: return 1;
+    case 2: return 0;
+    case 3: return 2;
+    default: return kDefaultEngine;
+  }
+}
+
 static MatParams window_params(const sllm_index& idx, const sllm_load_config& cfg, const PartJob& j, uint64_t k0,
                                uint64_t k1, uint64_t lo, uint64_t hi) {
   const bool check = cfg.verify && idx.block;
@@ -251,7 +262,7 @@ static MatParams window_params(const sllm_index& idx, const sllm_load_config& cf
   mp.expect = check ? j.d_expect : nullptr;
   mp.cs_out = check ? j.d_cs : nullptr;
   mp.bad = j.d_bad;
-  mp.engine = cfg.engine == 2 ? 0 : 1;
+  mp.engine = kernel_engine(cfg.engine);
   mp.n_peers = j.n_peers;
   for (uint32_t k = 0; k < j.n_peers; ++k) mp.peer[k] = j.peers[k];
   return mp;
@@ -396,7 +407,7 @@ static void verify_range(const sllm_index& idx, const sllm_load_config& cfg, Par
   mp.expect = j.d_expect;
   mp.cs_out = j.d_cs;
   mp.bad = j.d_bad;
-  mp.engine = cfg.engine == 2 ? 0 : 1;
+  mp.engine = kernel_engine(cfg.engine);
   launch(j, cfg.profile != 0, mp, MatKind::kChecksumOnly, cfg.ctas > 0 ? cfg.ctas : 0, st);
 }
 
@@ -629,7 +640,7 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (cfg.n_streams < 1 || cfg.n_streams > kMaxStreams) fail(SLLM_E_INVALID, "n_streams must be in 1..8");
   if (cfg.mode < SLLM_MODE_CE || cfg.mode > SLLM_MODE_SCATTER_ZC) fail(SLLM_E_INVALID, "unknown mode");
   if (cfg.profile < 0 || cfg.profile > 2) fail(SLLM_E_INVALID, "profile must be 0, 1 or 2");
-  if (cfg.engine < 0 || cfg.engine > 2) fail(SLLM_E_INVALID, "unknown kernel engine");
+  if (cfg.engine < 0 || cfg.engine > 3) fail(SLLM_E_INVALID, "unknown kernel engine");
   if (cfg.reserved) fail(SLLM_E_INVALID, "reserved config field must be 0");
   if (cfg.chunk_bytes % tile_for(*idx)) fail(SLLM_E_INVALID, "chunk size must be a multiple of the 64 KiB work tile");
   if (idx->block && cfg.chunk_bytes % idx->block) fail(SLLM_E_INVALID, "chunk size must be a multiple of the block size");

@@ -49,7 +49,7 @@ def check_against_oracle(res, idx, inv, lay, oparts, payloads, parts_loaded, cfg
             assert res.block_checksums(p).tolist() == lay.checksums[d]
 
 
-@pytest.mark.parametrize("engine", ["tma", "ldg"])
+@pytest.mark.parametrize("engine", ["tma", "ldg", "tma_store"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("chunk,streams", [(1 << 20, 1), (2 << 20, 2), (4 << 20, 3), (16 << 20, 2)])
 def test_toy_all_modes(mode, chunk, streams, engine):
@@ -65,7 +65,7 @@ def test_toy_all_modes(mode, chunk, streams, engine):
     check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
 
 
-@pytest.mark.parametrize("engine", ["tma", "ldg"])
+@pytest.mark.parametrize("engine", ["tma", "ldg", "tma_store"])
 @pytest.mark.parametrize("mode", MODES)
 def test_toy_align16_and_small_blocks(mode, engine):
     inv, seed = models.model_inventory("toy")
@@ -90,13 +90,13 @@ def test_random_checkpoints(seed):
     mode = MODES[seed % 4]
     chunk = B * int(rng.integers(1, 5)) if B >= 1 << 16 else 1 << 16
     cfg = sllm.LoadConfig(chunk_bytes=chunk, n_streams=int(rng.integers(1, 5)), mode=mode,
-                          ctas=int(rng.choice([0, 1, 5, 64])), engine=["tma", "ldg"][(seed // 4) % 2])
+                          ctas=int(rng.choice([0, 1, 5, 64])), engine=["tma", "ldg", "tma_store"][(seed // 4) % 3])
     n = len(idx.partitions)
     res = sllm.load(idx, bufs, {p: 0 for p in range(n)}, cfg)
     check_against_oracle(res, idx, inv, lay, oparts, payloads, list(range(n)), cfg)
 
 
-@pytest.mark.parametrize("engine", ["tma", "ldg"])
+@pytest.mark.parametrize("engine", ["tma", "ldg", "tma_store"])
 @pytest.mark.parametrize("mode", MODES)
 def test_fault_injection_names_block(mode, engine):
     """A flipped source byte in block j yields SLLM_E_CHECKSUM(0, j) -- the same
@@ -134,8 +134,9 @@ def test_verify_off_still_exact():
         check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
 
 
+@pytest.mark.parametrize("engine", ["tma", "ldg", "tma_store"])
 @pytest.mark.parametrize("mode", ["scatter_ce", "scatter_zc"])
-def test_scatter_canaries(mode):
+def test_scatter_canaries(mode, engine):
     """O9(b): guard bytes around every per-tensor destination stay untouched."""
     inv, seed = models.model_inventory("toy")
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
@@ -150,7 +151,8 @@ def test_scatter_canaries(mode):
         per_tensor[t.name] = arena[lo:lo + t.nbytes].view(dts[t.dtype]).view(t.shape)
         spans.append((lo, lo + t.nbytes))
         off = lo + ((t.nbytes + 15) // 16) * 16 + G
-    res = sllm.load_start(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode), None, per_tensor)
+    res = sllm.load_start(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode, engine=engine), None,
+                          per_tensor)
     res.wait()
     a = arena.cpu().numpy()
     mask = np.ones(a.size, bool)
@@ -228,7 +230,9 @@ def test_device_checksum_extreme_words():
         assert [int(v) & (2**64 - 1) for v in out.cpu().tolist()] == fletcher.block_checksums(x, 1 << 20)
 
 
-def test_materialise_device_matches_oracle():
+@pytest.mark.parametrize("engine", ["", "ldg", "tma", "tma_store"])
+def test_materialise_device_matches_oracle(engine, monkeypatch):
+    monkeypatch.setenv("SLLM_STANDALONE_ENGINE", engine)
     inv = models.llama2(512, 3, 1024, 128, vocab=2048, tp=2)
     idx, bufs = workloads.build_pinned(inv, 11, 4096, 1 << 16)
     lay, oparts, payloads = oracle_of(inv, 11, 4096, 1 << 16)
