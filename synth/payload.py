@@ -71,8 +71,10 @@ def build_csynth(force: bool = False) -> str:
     src = os.path.join(here, "csynth.c")
     if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
         import subprocess
+        tmp = f"{out}.tmp{os.getpid()}"  # several ranks may build at once: publish atomically
         subprocess.check_call(["gcc", "-O3", "-march=x86-64-v3", "-shared", "-fPIC", "-pthread",
-                               "-o", out, src])
+                               "-o", tmp, src])
+        os.replace(tmp, out)
     return out
 
 
