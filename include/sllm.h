@@ -191,6 +191,36 @@ SLLM_API sllm_status sllm_host_read_partition(const char* dir, const sllm_index*
                                      int32_t threads);
 
 /* ------------------------------------------------------------------------------------
+ * Pinned model cache: the DRAM tier as a pool of whole models with LRU eviction (PAPER.md
+ * P:578-579).  Thread-safe.
+ * ------------------------------------------------------------------------------------ */
+typedef struct sllm_cache sllm_cache;
+typedef struct {
+  uint64_t capacity, used;       /* bytes (each partition rounded up to 2 MiB)              */
+  uint64_t models;               /* resident (or being read) models                          */
+  uint64_t hits, misses, evictions;
+} sllm_cache_stats;
+/* capacity: bytes of host memory the cache may hold.  gpu >= 0: NUMA placement as
+ * sllm_host_alloc.  pin = 1: page-locked, device-mapped memory (a load source); pin = 0:
+ * plain page-aligned memory (host-only use). */
+SLLM_API sllm_status sllm_cache_create(uint64_t capacity, int32_t gpu, int32_t pin, sllm_cache** out);
+/* The model converted into <dir> (index.bin + part_<device>.bin).  Hit: the resident copy,
+ * marked most recently used.  Miss: its bytes are reserved by evicting least recently used
+ * models that nobody holds, then every partition is read with `io_threads` O_DIRECT
+ * readers (0 = 4) outside the cache lock; concurrent acquirers of the same model wait for
+ * that read.  Outputs (owned by the cache, valid until the matching release): *index, and
+ * *part_bufs = n_partitions host pointers (partition p at part_bufs[p]); *hit (may be
+ * NULL) = 1 on a hit.  The model is held (never evicted) until sllm_cache_release.
+ * SLLM_E_CAPACITY: the model does not fit even after evicting every unheld model. */
+SLLM_API sllm_status sllm_cache_acquire(sllm_cache* cache, const char* dir, int32_t io_threads,
+                                        const sllm_index** index, void* const** part_bufs, int32_t* hit);
+/* Drop one hold of <dir>; SLLM_E_LOOKUP if it is not held. */
+SLLM_API sllm_status sllm_cache_release(sllm_cache* cache, const char* dir);
+SLLM_API sllm_status sllm_cache_get_stats(sllm_cache* cache, sllm_cache_stats* out);
+/* Frees every resident model (held or not: the caller must have finished its loads). */
+SLLM_API void sllm_cache_destroy(sllm_cache* cache);
+
+/* ------------------------------------------------------------------------------------
  * Load (S:115 load()).
  * ------------------------------------------------------------------------------------ */
 typedef enum {

@@ -66,6 +66,14 @@ class IpcRegion(C.Structure):
                 ("reserved", C.c_int32)]
 
 
+class CacheStats(C.Structure):
+    _fields_ = [("capacity", C.c_uint64), ("used", C.c_uint64), ("models", C.c_uint64), ("hits", C.c_uint64),
+                ("misses", C.c_uint64), ("evictions", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 P = C.c_void_p
 PP = C.POINTER(C.c_void_p)
 U64 = C.c_uint64
@@ -103,6 +111,11 @@ SIGNATURES = {
     "sllm_comm_init_all": (S, [C.POINTER(C.c_int32), C.c_int32, PP]),
     "sllm_comm_init_peers": (S, [C.c_int32, C.c_int32, C.c_int32, PP, PP, U64, PP]),
     "sllm_comm_free": (None, [P]),
+    "sllm_cache_create": (S, [U64, C.c_int32, C.c_int32, PP]),
+    "sllm_cache_acquire": (S, [P, C.c_char_p, C.c_int32, PP, C.POINTER(PP), C.POINTER(C.c_int32)]),
+    "sllm_cache_release": (S, [P, C.c_char_p]),
+    "sllm_cache_get_stats": (S, [P, C.POINTER(CacheStats)]),
+    "sllm_cache_destroy": (None, [P]),
     "sllm_load_start": (S, [P, C.POINTER(LoadConfig), PP, C.POINTER(C.c_int32), PP, PP, PP, P, PP]),
     "sllm_load_files_start": (S, [P, C.POINTER(LoadConfig), C.c_char_p, C.POINTER(C.c_int32), PP, PP, PP, C.c_int32,
                                   PP]),

@@ -76,8 +76,9 @@ def _ptr_array(ptrs: Iterable[Optional[int]]) -> C.Array:
 class Index:
     """Owned handle to a parsed or planned index (sllm_index*)."""
 
-    def __init__(self, handle: int):
+    def __init__(self, handle: int, owned: bool = True):
         self._h = C.c_void_p(handle)
+        self._owned = owned  # False: borrowed from another owner (e.g. a PinnedCache entry)
         self._tensors: Optional[List[TensorInfo]] = None
         self._by_name: Optional[Dict[str, int]] = None
 
@@ -105,7 +106,8 @@ class Index:
 
     def close(self) -> None:
         if self._h and self._h.value:
-            lib().sllm_index_close(self._h)
+            if self._owned:
+                lib().sllm_index_close(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):
@@ -260,6 +262,43 @@ class HostBuffer:
     def __del__(self):
         try:
             self.free()
+        except Exception:
+            pass
+
+
+class PinnedCache:
+    """The pinned DRAM tier as a whole-model LRU cache (sllm_cache_*; PAPER.md P:578-579,
+    P:692).  ``acquire(dir)`` -> (Index, {partition: host pointer}) usable as
+    ``sllm.load`` sources; the model stays resident and unevictable until ``release(dir)``."""
+
+    def __init__(self, capacity: int, gpu: int = -1, pin: bool = True):
+        out = C.c_void_p()
+        check(lib().sllm_cache_create(int(capacity), gpu, int(pin), C.byref(out)))
+        self._h = out
+
+    def acquire(self, directory: str, io_threads: int = 0) -> Tuple["Index", Dict[int, int], bool]:
+        idx, bufs, hit = C.c_void_p(), C.POINTER(C.c_void_p)(), C.c_int32()
+        check(lib().sllm_cache_acquire(self._h, directory.encode(), io_threads, C.byref(idx), C.byref(bufs),
+                                       C.byref(hit)))
+        index = Index(idx.value, owned=False)
+        return index, {p: bufs[p] for p in range(len(index.partitions))}, bool(hit.value)
+
+    def release(self, directory: str) -> None:
+        check(lib().sllm_cache_release(self._h, directory.encode()))
+
+    def stats(self) -> dict:
+        st = _abi.CacheStats()
+        check(lib().sllm_cache_get_stats(self._h, C.byref(st)))
+        return st.as_dict()
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            lib().sllm_cache_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
         except Exception:
             pass
 

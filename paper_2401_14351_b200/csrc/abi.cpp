@@ -33,6 +33,14 @@ sllm_comm* sllm_comm_init_rank_internal(const void*, int32_t, int32_t, int32_t);
 void sllm_comm_init_all_internal(const int32_t*, int32_t, sllm_comm**);
 sllm_comm* sllm_comm_init_peers_internal(int32_t, int32_t, int32_t, void* const*, uint32_t* const*, uint64_t);
 void sllm_comm_free_internal(sllm_comm*);
+namespace sllm {
+sllm_cache* cache_create(uint64_t capacity, int gpu, int pin);
+void cache_acquire(sllm_cache* c, const char* dir, int io_threads, const sllm_index** index, void* const** bufs,
+                   int32_t* hit);
+void cache_release(sllm_cache* c, const char* dir);
+void cache_stats(sllm_cache* c, sllm_cache_stats* s);
+void cache_destroy(sllm_cache* c);
+}  // namespace sllm
 
 using namespace sllm;
 
@@ -306,6 +314,31 @@ sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void
 void sllm_comm_free(sllm_comm* c) {
   guard([&] { sllm_comm_free_internal(c); });
 }
+
+sllm_status sllm_cache_create(uint64_t capacity, int32_t gpu, int32_t pin, sllm_cache** out) {
+  return guard([&] {
+    if (!out) fail(SLLM_E_INVALID, "null out");
+    *out = cache_create(capacity, gpu, pin);
+  });
+}
+
+sllm_status sllm_cache_acquire(sllm_cache* c, const char* dir, int32_t io_threads, const sllm_index** index,
+                               void* const** part_bufs, int32_t* hit) {
+  return guard([&] { cache_acquire(c, dir, io_threads, index, part_bufs, hit); });
+}
+
+sllm_status sllm_cache_release(sllm_cache* c, const char* dir) {
+  return guard([&] { cache_release(c, dir); });
+}
+
+sllm_status sllm_cache_get_stats(sllm_cache* c, sllm_cache_stats* out) {
+  return guard([&] { cache_stats(c, out); });
+}
+
+void sllm_cache_destroy(sllm_cache* c) {
+  guard([&] { cache_destroy(c); });
+}
+
 
 sllm_status sllm_load_start(const sllm_index* idx, const sllm_load_config* cfg, const void* const* host_src,
                             const int32_t* gpu, void* const* dst_base, void* const* dst_tensor, void* const* stream,
