@@ -1,0 +1,113 @@
+"""Converter front-end for .safetensors checkpoints (paper_2401_14351_b200/formats.py).
+
+The input files are written by the independent ``safetensors`` package; the converted
+checkpoint is read back with the oracle's own index reader (oracle/index.py), the layout is
+re-derived by the oracle's layout algorithm from the index's tensor order, and every
+tensor's bytes are compared with what ``safetensors.safe_open`` reads -- padding must be
+zero, block checksums must equal the oracle's."""
+import os
+
+import numpy as np
+import pytest
+
+st_numpy = pytest.importorskip("safetensors.numpy")
+from safetensors import safe_open  # noqa: E402
+
+from paper_2401_14351_b200 import _abi, formats  # noqa: E402
+from oracle import fletcher, index as oindex, layout as olayout  # noqa: E402
+
+
+def _tensors(seed):
+    rng = np.random.default_rng(seed)
+    return {
+        "model.embed.weight": rng.standard_normal((300, 64)).astype(np.float16),
+        "model.layers.0.q.weight": rng.standard_normal((64, 64)).astype(np.float32),
+        "model.layers.0.norm.bias": rng.standard_normal((33,)).astype(np.float16),   # 66 B
+        "model.scale": np.array(1.5, dtype=np.float16),                              # scalar, 2 B
+        "model.ids": rng.integers(-2**40, 2**40, size=(17,), dtype=np.int64),
+        "model.qweight": rng.integers(-128, 127, size=(40, 24), dtype=np.int8),
+        "model.mask": rng.integers(0, 255, size=(9, 3), dtype=np.uint8),
+    }
+
+
+def _check(out_dir, files, device_of, A, B):
+    blob = open(os.path.join(out_dir, "index.bin"), "rb").read()
+    lay = oindex.read(blob)                       # oracle reader: every FormatError check
+    ref = olayout.plan([(e.name, e.device, e.dtype, e.shape, e.size) for e in lay.entries], A, B)
+    assert [(e.name, e.offset) for e in ref.entries] == [(e.name, e.offset) for e in lay.entries]
+    assert ref.partitions == lay.partitions
+    arrays = {}
+    for f in files:
+        with safe_open(f, framework="numpy") as h:
+            for k in h.keys():
+                arrays[k] = h.get_tensor(k)
+    assert sorted(arrays) == sorted(e.name for e in lay.entries)
+    for d in lay.devices():
+        part = np.fromfile(os.path.join(out_dir, f"part_{d}.bin"), dtype=np.uint8)
+        assert part.size == lay.partitions[d]
+        covered = np.zeros(part.size, bool)
+        for e in lay.entries:
+            if e.device != d:
+                continue
+            assert e.device == device_of(e.name)
+            want = np.ascontiguousarray(arrays[e.name]).reshape(-1).view(np.uint8)
+            assert tuple(e.shape) == tuple(arrays[e.name].shape)
+            assert np.array_equal(part[e.offset:e.offset + e.size], want), e.name
+            covered[e.offset:e.offset + e.size] = True
+        assert not part[~covered].any()          # Q3: padding is 0x00
+        assert lay.checksums[d] == fletcher.block_checksums(part, B)
+
+
+def test_single_file(tmp_path):
+    f = str(tmp_path / "model.safetensors")
+    st_numpy.save_file(_tensors(0), f)
+    out = str(tmp_path / "ckpt")
+    n = formats.convert_safetensors([f], out, align=4096, block=1 << 16, model_id="st-test")
+    assert n == 7
+    _check(out, [f], lambda name: 0, 4096, 1 << 16)
+
+
+def test_sharded_files_to_two_partitions(tmp_path):
+    t = _tensors(1)
+    names = sorted(t)
+    f1, f2 = str(tmp_path / "model-00001-of-00002.safetensors"), str(tmp_path / "model-00002-of-00002.safetensors")
+    st_numpy.save_file({k: t[k] for k in names[:4]}, f1)
+    st_numpy.save_file({k: t[k] for k in names[4:]}, f2)
+    dev = lambda name: 1 if "layers" in name or "mask" in name else 0  # noqa: E731
+    out = str(tmp_path / "ckpt")
+    formats.convert_safetensors([f1, f2], out, device_of=dev, align=256, block=1 << 12)
+    _check(out, [f1, f2], dev, 256, 1 << 12)
+
+
+def test_rejects_unsupported_dtype_and_duplicates(tmp_path):
+    f = str(tmp_path / "f64.safetensors")
+    st_numpy.save_file({"w": np.zeros((4,), np.float64)}, f)
+    with pytest.raises(_abi.SllmError) as ex:
+        formats.convert_safetensors([f], str(tmp_path / "o1"))
+    assert ex.value.status == _abi.E_CONVERSION
+    g = str(tmp_path / "g.safetensors")
+    st_numpy.save_file({"w": np.zeros((4,), np.float16)}, g)
+    with pytest.raises(_abi.SllmError) as ex:        # the same name in two shards
+        formats.convert_safetensors([g, g], str(tmp_path / "o2"))
+    assert ex.value.status == _abi.E_CONVERSION
+
+
+def test_cli_convert_and_info(tmp_path):
+    import json
+    import subprocess
+    import sys
+    f = str(tmp_path / "m.safetensors")
+    st_numpy.save_file(_tensors(2), f)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {**os.environ, "PYTHONPATH": root}
+    out = str(tmp_path / "ckpt")
+    r = subprocess.run([sys.executable, "-m", "paper_2401_14351_b200", "convert", "--out", out, "--block", "65536", f],
+                       capture_output=True, text=True, env=env)
+    assert r.returncode == 0, r.stderr
+    assert json.loads(r.stdout)["converted_tensors"] == 7
+    _check(out, [f], lambda name: 0, 4096, 1 << 16)
+    r = subprocess.run([sys.executable, "-m", "paper_2401_14351_b200", "info", out], capture_output=True, text=True,
+                       env=env)
+    assert r.returncode == 0, r.stderr
+    info = json.loads(r.stdout)
+    assert info["n_tensors"] == 7 and len(info["partitions"]) == 1
