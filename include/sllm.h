@@ -270,6 +270,9 @@ typedef struct {
   int32_t bad_partition;       /* -1 when OK                                                */
   int32_t mode;
   uint64_t bad_block;          /* UINT64_MAX when OK                                        */
+  uint64_t storage_bytes;      /* file tier: bytes read from the partition files            */
+  uint64_t t_storage_wait_ns_max; /* file tier: longest time a partition's GPU worker waited for
+                                     storage (0 = storage never the bottleneck)              */
 } sllm_load_report;
 
 /* Communicator for SLLM_FANOUT_BCAST.  One process per GPU: rank 0 calls

@@ -66,6 +66,7 @@ struct FileSource {
   std::string error;
   std::vector<std::thread> io;
   uint64_t bytes_read = 0;
+  uint64_t wait_ns = 0;  // time the GPU worker spent blocked on storage (a per-tier time)
 };
 
 static void read_window(FileSource& f, uint64_t w, uint8_t* dst) {
@@ -158,7 +159,12 @@ FileSourcePtr file_source_open(const std::string& path, uint64_t length, uint64_
 const uint8_t* file_source_window(FileSource& f, uint64_t w) {
   const int s = (int)(w % (uint64_t)f.R);
   std::unique_lock<std::mutex> lk(f.mu);
-  f.cv.wait(lk, [&] { return !f.error.empty() || f.ready[s] == w + 1; });
+  if (f.error.empty() && f.ready[s] != w + 1) {
+    const auto t0 = std::chrono::steady_clock::now();
+    f.cv.wait(lk, [&] { return !f.error.empty() || f.ready[s] == w + 1; });
+    f.wait_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0)
+                     .count();
+  }
   if (!f.error.empty()) fail(SLLM_E_IO, f.error);
   return static_cast<const uint8_t*>(f.slots[s]);
 }
@@ -176,6 +182,11 @@ void file_source_consumed(FileSource& f, uint64_t w, cudaStream_t st) {
 uint64_t file_source_bytes(FileSource& f) {
   std::lock_guard<std::mutex> g(f.mu);
   return f.bytes_read;
+}
+
+uint64_t file_source_wait_ns(FileSource& f) {
+  std::lock_guard<std::mutex> g(f.mu);
+  return f.wait_ns;
 }
 
 }  // namespace sllm

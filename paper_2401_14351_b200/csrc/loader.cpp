@@ -117,6 +117,7 @@ struct PartJob {
   uint64_t t_issue_ns = 0;
   float t_dev_ms = 0.f;
   uint64_t chunks = 0, launches = 0, copies = 0, transferred = 0, fanout = 0;
+  uint64_t storage_bytes = 0, storage_wait_ns = 0;  // file tier
   // profile: (start, end) event pairs around kernel launches / copies
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev, cev;
   uint64_t kernel_bytes = 0;
@@ -572,6 +573,10 @@ static void run_job(sllm_load* L, PartJob& j) {
   if (j.origin) gate_open_device(s0, j.gate);  // releases the caller's stream on the device
   j.t_issue_ns = now_ns() - t0;
   SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
+  if (j.fsrc) {
+    j.storage_bytes = file_source_bytes(*j.fsrc);
+    j.storage_wait_ns = file_source_wait_ns(*j.fsrc);
+  }
   j.fsrc.reset();  // file tier: readers are done, slots go back to the pinned pool
   uint64_t tail[2] = {};
   SLLM_CUDA(cudaMemcpy(tail, j.d_bad, 16, cudaMemcpyDeviceToHost));  // first failing block, peer-wait result
@@ -797,6 +802,8 @@ static void join_load(sllm_load* L) {
     r.t_kernel_ms_sum += j.kernel_ms;
     r.t_copy_ms_sum += j.copy_ms;
     r.kernel_bytes += j.kernel_bytes;
+    r.storage_bytes += j.storage_bytes;
+    r.t_storage_wait_ns_max = std::max(r.t_storage_wait_ns_max, j.storage_wait_ns);
     if (j.status != SLLM_OK && st == SLLM_OK) {
       st = j.status;
       err = j.error;

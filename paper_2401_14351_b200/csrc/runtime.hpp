@@ -58,6 +58,7 @@ FileSourcePtr file_source_open(const std::string& path, uint64_t length, uint64_
 const uint8_t* file_source_window(FileSource& f, uint64_t w);        // blocks until window w is in its slot
 void file_source_consumed(FileSource& f, uint64_t w, cudaStream_t s);  // slot reusable once s passes here
 uint64_t file_source_bytes(FileSource& f);
+uint64_t file_source_wait_ns(FileSource& f);  // worker time blocked waiting for storage
 
 // ---- stream gates (gate.cpp) -------------------------------------------------------
 struct Gate {

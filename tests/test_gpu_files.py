@@ -44,6 +44,7 @@ def test_toy_from_files(tmp_path, mode, io_threads):
     res = sllm.load_files(idx, str(tmp_path), {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode),
                           io_threads=io_threads)
     assert res.report["transferred_bytes"] == 13_594_624
+    assert res.report["storage_bytes"] == 13_594_624  # every partition byte read from storage once
     check(res, inv, payloads, lay, [0])
 
 
