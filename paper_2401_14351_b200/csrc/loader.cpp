@@ -343,12 +343,13 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
         SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
         // K4 runs per verification span of landed windows: up to kVerifyBytes per launch
         // (few, long launches that keep every SM streaming), and once the pending span is
-        // at least as long as what is still to come, at once -- spans halve towards the end,
-        // so the tail after the last copy is about one window's K4.  The copies never wait.
+        // at least kVerifyTailBytes and as long as what is still to come, at once -- spans
+        // shrink towards the end, so the tail after the last copy is one K4 of at most
+        // ~kVerifyTailBytes (~0.1 ms at HBM rate).  The copies never wait.
         if (P.v_k1 == P.v_k0) P.v_k0 = k0;
         P.v_k1 = k1;
         const uint64_t pending = std::min(P.v_k1 * C, L) - P.v_k0 * C;
-        if (last || pending >= kVerifyBytes || pending >= L - hi) {
+        if (last || pending >= kVerifyBytes || (pending >= kVerifyTailBytes && pending >= L - hi)) {
           MatParams vp = window_params(idx, cfg, j, P.v_k0, P.v_k1, P.v_k0 * C, std::min(P.v_k1 * C, L));
           vp.src = j.dst_base;
           vp.src_origin = 0;
