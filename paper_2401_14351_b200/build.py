@@ -55,18 +55,27 @@ def _headers():
         [os.path.join(ROOT, "include", "sllm.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+# (nvcc splits -Xcompiler values on commas: one sanitizer per flag)
+SAN_FLAGS = "-fsanitize=address,-fsanitize=undefined,-fno-omit-frame-pointer,-fno-sanitize-recover=all"
+
+
+def build(force: bool = False, verbose: bool = False, sanitize: bool = False) -> str:
+    """sanitize=True: an AddressSanitizer + UBSan build of the host code (kernels unchanged)
+    at build/sllm_asan/libsllm_asan.so, for tests/test_sanitizers.py -- never the product."""
     srcs = sources()
+    out = os.path.join(ROOT, "build", "sllm_asan", "libsllm_asan.so") if sanitize else OUT
+    bdir = os.path.join(ROOT, "build", "sllm_asan") if sanitize else BUILD
     newest = max(os.path.getmtime(p) for p in srcs + _headers() + [__file__])
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
-        return OUT
-    os.makedirs(BUILD, exist_ok=True)
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
+        return out
+    os.makedirs(bdir, exist_ok=True)
     nvcc = _nvcc()
-    common = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",
+    host = "-fPIC,-O3,-fvisibility=hidden" if not sanitize else "-fPIC,-O1,-g,-fvisibility=hidden," + SAN_FLAGS
+    common = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", host,
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()]
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
         cmd = [nvcc, *common, "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
@@ -79,14 +88,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
-    tmp = f"{OUT}.tmp{os.getpid()}"
+    tmp = f"{out}.tmp{os.getpid()}"
     cmd = [nvcc, "-shared", *ARCH, "-cudart", "static", "-o", tmp, *objs, "-ldl", "-lpthread", "-lrt",
-           "-Xlinker", "--exclude-libs,ALL"]
+           "-Xlinker", "--exclude-libs,ALL"] + (["-Xcompiler", SAN_FLAGS] if sanitize else [])
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

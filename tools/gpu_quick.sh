@@ -1,6 +1,6 @@
-# quick check: GPU tests + CE bench + in-pipeline ncu capture of the K4 verification launch
+# quick check: GPU tests + CE bench (+ NCU=1: in-pipeline ncu capture of a K4 verification launch + launch list)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 for m in ${BENCH_MODES:-ce}; do
   timeout 600 python bench.py --mode $m --steps 5 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench_$m.json 2> gpurun_out/bench_$m.err
 done
