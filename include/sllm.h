@@ -298,6 +298,9 @@ SLLM_API sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_com
  *                   overwritten by the next one), so back-to-back loads need no host barrier.
  *   timeout_ms    : how long a rank waits for its peers' completion signals before the
  *                   load fails with SLLM_E_PEER (0 = 60000).
+ * A P2P load completes only when every rank's load has run, so several ranks driven from
+ * one process must not pass the same caller stream (its gate would order them one after
+ * the other and the first would wait for the others until the timeout).
  * The handle owns its streams; sllm_comm_free releases them (never the replicas). */
 SLLM_API sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
                                           uint32_t* const* peer_signal, uint64_t timeout_ms, sllm_comm** out);
@@ -336,10 +339,13 @@ SLLM_API sllm_status sllm_load_start(const sllm_index* index, const sllm_load_co
  * with O_DIRECT reads, each slot's window is copied / verified / scattered exactly
  * as in sllm_load_start, and a slot is refilled once the GPU has consumed it.
  *   gpu[p] : CUDA ordinal for partition p, or < 0 to skip that partition.
- *   other arguments as in sllm_load_start (no fan-out).  SLLM_E_IO names the file. */
+ *   comm   : as in sllm_load_start: with a fan-out (replicated checkpoint) this rank reads
+ *            only its slice of part_<d>.bin from storage and the rest arrives over NVLink,
+ *            so the group reads every byte from storage once.
+ *   other arguments as in sllm_load_start.  SLLM_E_IO names the file. */
 SLLM_API sllm_status sllm_load_files_start(const sllm_index* index, const sllm_load_config* cfg, const char* dir,
                                            const int32_t* gpu, void* const* dst_base, void* const* dst_tensor,
-                                           void* const* stream, int32_t io_threads, sllm_load** out);
+                                           void* const* stream, int32_t io_threads, sllm_comm* comm, sllm_load** out);
 
 /* Block until every chunk (and fan-out round) has landed and been verified.  Returns
  * SLLM_E_CHECKSUM with rep->bad_partition / rep->bad_block naming the first failing

@@ -522,9 +522,11 @@ def load_start(index: Index, sources: Dict[int, object], gpus: Dict[int, int], c
 
 def load_files(index: Index, directory: str, gpus: Dict[int, int], config: Optional[LoadConfig] = None,
                io_threads: int = 0, wait: bool = True, stream_of_caller: bool = True,
-               bases: Optional[Dict[int, object]] = None, per_tensor: Optional[Dict[str, object]] = None) -> LoadResult:
+               bases: Optional[Dict[int, object]] = None, per_tensor: Optional[Dict[str, object]] = None,
+               comm: Optional[Comm] = None) -> LoadResult:
     """The full multi-tier pipeline from <directory>/part_<device>.bin (sllm_load_files_start):
-    O_DIRECT readers -> pinned slot ring -> GPU, for the partitions listed in ``gpus``."""
+    O_DIRECT readers -> pinned slot ring -> GPU, for the partitions listed in ``gpus``.  With
+    a fan-out config and ``comm`` (replicated checkpoint) this rank reads only its slice."""
     import torch
     cfg = config or LoadConfig()
     if bases is None and per_tensor is None:
@@ -544,7 +546,7 @@ def load_files(index: Index, directory: str, gpus: Dict[int, int], config: Optio
     out = C.c_void_p()
     ccfg = cfg.to_c()
     check(lib().sllm_load_files_start(index.handle, C.byref(ccfg), directory.encode(), gpu, dst_base, dst_tensor, st,
-                                      io_threads, C.byref(out)))
+                                      io_threads, comm.handle if comm else None, C.byref(out)))
     tensors: Dict[str, object] = {}
     tdt = _torch_dtypes()
     for t in index.tensors:

@@ -351,10 +351,10 @@ sllm_status sllm_load_start(const sllm_index* idx, const sllm_load_config* cfg, 
 
 sllm_status sllm_load_files_start(const sllm_index* idx, const sllm_load_config* cfg, const char* dir, const int32_t* gpu,
                                   void* const* dst_base, void* const* dst_tensor, void* const* stream, int32_t io_threads,
-                                  sllm_load** out) {
+                                  sllm_comm* comm, sllm_load** out) {
   return guard([&] {
     if (!out || !dir) fail(SLLM_E_INVALID, "null argument");
-    *out = sllm_load_create_internal(idx, cfg, nullptr, gpu, dst_base, dst_tensor, stream, nullptr, dir, io_threads);
+    *out = sllm_load_create_internal(idx, cfg, nullptr, gpu, dst_base, dst_tensor, stream, comm, dir, io_threads);
   });
 }
 

@@ -52,7 +52,7 @@ static void pool_release(const std::vector<void*>& slots, uint64_t bytes) {
 
 struct FileSource {
   std::string path;
-  uint64_t length = 0, window = 0, nwin = 0;
+  uint64_t base = 0, length = 0, window = 0, nwin = 0;  // window w = file bytes [base + w*window, ...) < length
   int R = 0;
   int fd_direct = -1, fd_buf = -1;
   std::vector<void*> slots;
@@ -70,7 +70,7 @@ struct FileSource {
 };
 
 static void read_window(FileSource& f, uint64_t w, uint8_t* dst) {
-  const uint64_t lo = w * f.window, hi = std::min(lo + f.window, f.length);
+  const uint64_t lo = f.base + w * f.window, hi = std::min(lo + f.window, f.length);
   const uint64_t direct_end = f.fd_direct >= 0 ? f.length / 4096 * 4096 : 0;
   uint64_t pos = lo;
   while (pos < hi) {
@@ -100,7 +100,7 @@ static void io_main(FileSource* f, int gpu) {
       {
         std::lock_guard<std::mutex> g(f->mu);
         f->ready[s] = w + 1;
-        f->bytes_read += std::min(f->window, f->length - w * f->window);
+        f->bytes_read += std::min(f->window, f->length - f->base - w * f->window);
       }
       f->cv.notify_all();
     }
@@ -132,12 +132,14 @@ void FileSourceDeleter::operator()(FileSource* f) const {
   delete f;
 }
 
-FileSourcePtr file_source_open(const std::string& path, uint64_t length, uint64_t window, int io_threads, int gpu) {
+FileSourcePtr file_source_open(const std::string& path, uint64_t lo, uint64_t length, uint64_t window, int io_threads,
+                               int gpu) {
   FileSourcePtr f(new FileSource);
   f->path = path;
+  f->base = lo;
   f->length = length;
   f->window = window;
-  f->nwin = ceil_div(length, window);
+  f->nwin = length > lo ? ceil_div(length - lo, window) : 0;
   f->fd_buf = ::open(path.c_str(), O_RDONLY);
   if (f->fd_buf < 0) fail(SLLM_E_IO, "cannot open " + path + ": " + strerror(errno));
   struct stat st;

@@ -452,7 +452,8 @@ static void run_job(sllm_load* L, PartJob& j) {
   const uint64_t nch_all = std::max<uint64_t>(1, ceil_div(pr.length, cfg.chunk_bytes));
   P.slot_bytes = std::min(P.window, nch_all) * cfg.chunk_bytes;
   P.nslot = (int)std::min<uint64_t>((uint64_t)P.nslot, ceil_div(nch_all, P.window));
-  if (!j.file.empty()) j.fsrc = file_source_open(j.file, pr.length, P.window * cfg.chunk_bytes, j.io_threads, j.gpu);
+  if (!j.file.empty())  // (a replicated load reads only its slice [lo, hi) from storage)
+    j.fsrc = file_source_open(j.file, j.lo, j.hi, P.window * cfg.chunk_bytes, j.io_threads, j.gpu);
   SLLM_CUDA(cudaEventCreateWithFlags(&P.copied, cudaEventDisableTiming));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
     P.freed.resize(P.nslot);
@@ -665,7 +666,6 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
     fail(SLLM_E_INVALID, "unknown fan-out");
   }
   if ((!host_src && !dir) || !gpu) fail(SLLM_E_INVALID, "null host_src / gpu array");
-  if (dir && cfg.fanout != SLLM_FANOUT_NONE) fail(SLLM_E_INVALID, "the file tier does not combine with the fan-out");
   if (scatter && !dst_tensor) fail(SLLM_E_INVALID, "scatter modes need dst_tensor");
   if (!scatter && !dst_base) fail(SLLM_E_INVALID, "contiguous modes need dst_base");
 

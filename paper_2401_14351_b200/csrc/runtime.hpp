@@ -54,8 +54,10 @@ struct FileSourceDeleter {
 };
 using FileSourcePtr = std::unique_ptr<FileSource, FileSourceDeleter>;
 // Start `io_threads` O_DIRECT readers filling a ring of pinned `window`-byte slots with
-// windows of the partition file at `path` (length bytes).
-FileSourcePtr file_source_open(const std::string& path, uint64_t length, uint64_t window, int io_threads, int gpu);
+// windows of the partition file at `path`: window w = bytes [lo + w*window, ...) below
+// `length` (lo > 0: a replicated load's slice).
+FileSourcePtr file_source_open(const std::string& path, uint64_t lo, uint64_t length, uint64_t window, int io_threads,
+                               int gpu);
 const uint8_t* file_source_window(FileSource& f, uint64_t w);        // blocks until window w is in its slot
 void file_source_consumed(FileSource& f, uint64_t w, cudaStream_t s);  // slot reusable once s passes here
 uint64_t file_source_bytes(FileSource& f);

@@ -203,3 +203,54 @@ def test_p2p_fanout_two_processes_ipc(mode):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok, _ in out), out
+
+
+@pytest.mark.parametrize("R,mode,chunk", [(2, "ce", 1 << 20), (3, "zerocopy", 1 << 20), (3, "ce", 2 << 20)])
+def test_p2p_from_files_reads_each_byte_once(tmp_path, R, mode, chunk):
+    """Replicated checkpoint straight from its partition file (file tier + fused fan-out):
+    rank r reads only its slice from storage -- the group reads every byte once -- and every
+    replica still ends equal to P_0."""
+    inv, seed = models.model_inventory("toy")
+    payloads = [payload.payload_bytes(seed, e, t.nbytes) for e, t in enumerate(inv)]
+    sllm.convert([(t.name, t.device, t.dtype, t.shape, p.ctypes.data) for t, p in zip(inv, payloads)],
+                 str(tmp_path), 4096, 1 << 20, "toy")
+    lay, oparts, _ = oracle_of(inv, seed)
+    idx = sllm.Index.open(str(tmp_path / "index.bin"))
+    L = idx.partitions[0].length
+    slices = sllm.replica_slices(L, chunk, R)
+    bases, sigs, comms = group(R, L)
+    cfg = sllm.LoadConfig(chunk_bytes=chunk, mode=mode, fanout="p2p")
+    for _ in range(2):
+        for b in bases:
+            b.fill_(0x3C)
+        torch.cuda.synchronize()
+        # (all ranks share this thread's stream: ordering them on it would serialise the group,
+        # so the caller-stream gate is off -- each process of a real group has its own stream)
+        results = [sllm.load_files(idx, str(tmp_path), {0: 0}, cfg, io_threads=2, wait=False, stream_of_caller=False,
+                                   bases={0: bases[r]}, per_tensor={}, comm=comms[r]) for r in range(R)]
+        reports = [res.wait() for res in results]
+        for r, rep in enumerate(reports):
+            lo, hi = slices[r]
+            assert rep["storage_bytes"] == hi - lo
+            assert np.array_equal(bases[r].cpu().numpy(), oparts[0]), r
+            assert results[r].block_checksums(0).tolist() == lay.checksums[0]
+        assert sum(rep["storage_bytes"] for rep in reports) == L
+        del results
+    for c in comms:
+        c.free()
+
+
+def test_bcast_from_files_single_rank(tmp_path):
+    inv, seed = models.model_inventory("toy")
+    payloads = [payload.payload_bytes(seed, e, t.nbytes) for e, t in enumerate(inv)]
+    sllm.convert([(t.name, t.device, t.dtype, t.shape, p.ctypes.data) for t, p in zip(inv, payloads)],
+                 str(tmp_path), 4096, 1 << 20, "toy")
+    lay, oparts, _ = oracle_of(inv, seed)
+    idx = sllm.Index.open(str(tmp_path / "index.bin"))
+    comm = sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, 0)
+    res = sllm.load_files(idx, str(tmp_path), {0: 0}, sllm.LoadConfig(chunk_bytes=2 << 20, fanout="bcast"),
+                          comm=comm)
+    assert res.report["storage_bytes"] == idx.partitions[0].length
+    assert np.array_equal(res._keep[3][0].cpu().numpy(), oparts[0])
+    del res
+    comm.free()
