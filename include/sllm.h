@@ -227,7 +227,10 @@ typedef enum {
   SLLM_MODE_CE = 0,         /* copy engine per chunk into base+off, then checksum kernel     */
   SLLM_MODE_ZEROCOPY = 1,   /* SM-issued 16 B reads of host-mapped memory -> base+off, fused checksum */
   SLLM_MODE_SCATTER_CE = 2, /* copy engine into a staging ring, then index-driven scatter kernel */
-  SLLM_MODE_SCATTER_ZC = 3  /* SM-issued host reads scattered straight into per-tensor buffers */
+  SLLM_MODE_SCATTER_ZC = 3, /* SM-issued host reads scattered straight into per-tensor buffers */
+  SLLM_MODE_AUTO = 4        /* contiguous: ZEROCOPY when every partition (fan-out: slice) this
+                               call moves is < 256 MiB and device-mapped, else CE; the report's
+                               `mode` says which ran */
 } sllm_mode;
 
 /* Replicated checkpoint (one partition, every GPU gets a full replica): rank r of n moves

@@ -645,7 +645,12 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (cfg.chunk_bytes == 0) cfg.chunk_bytes = 16ull << 20;
   if (cfg.n_streams == 0) cfg.n_streams = 2;
   if (cfg.n_streams < 1 || cfg.n_streams > kMaxStreams) fail(SLLM_E_INVALID, "n_streams must be in 1..8");
-  if (cfg.mode < SLLM_MODE_CE || cfg.mode > SLLM_MODE_SCATTER_ZC) fail(SLLM_E_INVALID, "unknown mode");
+  if (cfg.mode < SLLM_MODE_CE || cfg.mode > SLLM_MODE_AUTO) fail(SLLM_E_INVALID, "unknown mode");
+  // AUTO: the copy engine unless every job moves less than kAutoZeroCopyBytes over PCIe from
+  // device-mapped memory -- then the zero-copy kernel, whose lower fixed cost wins for small
+  // loads (measured crossover).  Resolved below once the jobs are known.
+  const bool auto_mode = cfg.mode == SLLM_MODE_AUTO;
+  if (auto_mode) cfg.mode = SLLM_MODE_CE;
   if (cfg.profile < 0 || cfg.profile > 2) fail(SLLM_E_INVALID, "profile must be 0, 1 or 2");
   if (cfg.engine < 0 || cfg.engine > 3) fail(SLLM_E_INVALID, "unknown kernel engine");
   if (cfg.reserved) fail(SLLM_E_INVALID, "reserved config field must be 0");
@@ -732,6 +737,11 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
     L->jobs.push_back(std::move(j));
   }
   // busy set
+  if (auto_mode) {
+    bool zc = !L->jobs.empty();
+    for (auto& j : L->jobs) zc = zc && (j.hi - j.lo) < kAutoZeroCopyBytes && (j.src_dev || !j.file.empty());
+    if (zc) cfg.mode = L->cfg.mode = SLLM_MODE_ZEROCOPY;
+  }
   {
     std::lock_guard<std::mutex> g(g_busy_mu);
     std::vector<const void*> keys;

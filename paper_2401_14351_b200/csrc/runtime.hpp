@@ -24,6 +24,7 @@ constexpr uint32_t kTile = 64u << 10;  // bytes per kernel work tile
 constexpr uint64_t kWindowBytes = 64ull << 20;   // min bytes per copy submission / kernel launch
 constexpr uint64_t kVerifyBytes = 2048ull << 20;  // CE mode: max bytes per verification launch
 constexpr uint64_t kVerifyTailBytes = 512ull << 20;  // CE mode: min span once the load's end is near
+constexpr uint64_t kAutoZeroCopyBytes = 256ull << 20;  // SLLM_MODE_AUTO: zero-copy below this per job
 constexpr int kDefaultEngine = 1;  // MatParams.engine of sllm_load_config.engine == 0
 constexpr uint64_t kScatterWindowBytes = 256ull << 20;  // SCATTER_CE: bytes per staging slot / K3 launch
 

@@ -287,3 +287,23 @@ def test_opt67b_full_size_sampled():
             assert np.array_equal(got[:n].cpu().numpy(), payload.payload_bytes(seed, e, t.nbytes)[:n])
         del res
         torch.cuda.empty_cache()
+
+
+def test_auto_mode_picks_by_size():
+    """SLLM_MODE_AUTO: zero-copy for a small checkpoint, the copy engine for one above the
+    256 MiB crossover; both exact."""
+    inv, seed = models.model_inventory("toy")
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    lay, oparts, payloads = oracle_of(inv, seed, 4096, 1 << 20)
+    res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(mode="auto"))
+    assert res.report["mode"] == 1  # ZEROCOPY
+    check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], sllm.LoadConfig(mode="zerocopy"))
+    big = models.llama2(1024, 12, 4096, 1024, vocab=32000)  # ~0.4 GB, one partition
+    idx2, bufs2 = workloads.build_pinned(big, 9, 4096, 1 << 20)
+    res2 = sllm.load(idx2, bufs2, {0: 0}, sllm.LoadConfig(mode="auto", chunk_bytes=64 << 20))
+    assert idx2.partitions[0].length >= 256 << 20 and res2.report["mode"] == 0  # CE
+    assert np.array_equal(res2.block_checksums(0), idx2.block_checksums(0))
+    for e in (0, len(big) - 1):
+        t = big[e]
+        got = res2.tensors[t.name].reshape(-1).view(torch.uint8)[:4096].cpu().numpy()
+        assert np.array_equal(got, payload.payload_bytes(9, e, t.nbytes)[:4096])
