@@ -486,7 +486,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   SLLM_CUDA(cudaMemsetAsync(j.d_acc, 0, acc_bytes, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_cs, 0, tab_bytes, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_bad, 0xFF, 8, s0));
-  SLLM_CUDA(cudaMemsetAsync(j.d_err, 0, 4, s0));
+  SLLM_CUDA(cudaMemsetAsync(j.d_err, 0, 8, s0));  // (the 16-byte result read covers it all)
   if (nb) SLLM_CUDA(cudaMemcpyAsync(j.d_expect, pr.checksums.data(), nb * 8, cudaMemcpyHostToDevice, s0));
   SLLM_CUDA(cudaEventRecord(j.ev[0], s0));
   if (p2p) {  // no store into a peer replica before every peer is done verifying the previous load
