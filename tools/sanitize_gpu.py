@@ -23,8 +23,11 @@ def main():
     pl = [payload.payload_bytes(seed, e, t.nbytes) for e, t in enumerate(inv)]
     lay, parts = olayout.convert([(t.name, t.device, t.dtype, t.shape, p) for t, p in zip(inv, pl)], 4096, 1 << 20)
     n = 0
+    only = os.environ.get("SANITIZE_ONLY")  # e.g. "zerocopy:tma" -- one load, nothing else
     for engine in ("tma", "ldg", "tma_store"):
         for mode in ("ce", "zerocopy", "scatter_ce", "scatter_zc"):
+            if only and only != f"{mode}:{engine}":
+                continue
             res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=2 << 20, mode=mode, engine=engine))
             for e, t in enumerate(inv):
                 got = res.tensors[t.name].reshape(-1).view(torch.uint8).cpu().numpy()
@@ -32,6 +35,9 @@ def main():
             assert res.block_checksums(0).tolist() == lay.checksums[0]
             n += 1
             del res
+    if only:
+        print(f"sanitize_gpu ok: {n} load ({only})")
+        return
     # P2P fan-out, 2 ranks on this GPU
     L = idx.partitions[0].length
     bases = [torch.empty(L, dtype=torch.uint8, device="cuda") for _ in range(2)]
