@@ -48,9 +48,10 @@ def parse():
     ap.add_argument("--all-partitions", action="store_true",
                     help="load every partition of a multi-partition config onto this rank's GPU (e.g. the whole "
                          "LLaMA-2-70B TP8 checkpoint on one B200)")
-    ap.add_argument("--fanout", default="none", choices=["none", "bcast", "p2p"],
+    ap.add_argument("--fanout", default="none", choices=["none", "bcast", "allgather", "p2p"],
                     help="replicated checkpoint: every rank ends with a full replica; rank r reads slice r over "
-                         "PCIe and the rest arrives over NVLink (bcast: NCCL broadcasts, p2p: fused peer stores)")
+                         "PCIe and the rest arrives over NVLink (bcast: NCCL broadcasts, allgather: in-place NCCL "
+                         "all-gather per round of round-robin chunks, p2p: fused peer stores)")
     ap.add_argument("--cpu-sample-gib", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-standalone", action="store_true")
@@ -239,14 +240,20 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1):
     return max(out.values()), out
 
 
-def standalone_hbm(idx, torch, sllm, reps=5):
-    """K4 (checksum) and K3 (scatter + checksum) on a >= 1 GiB device-resident partition
-    image, timed with CUDA events on the launching stream (HBM roofline)."""
-    p = 0
+def standalone_hbm(idx, bufs, torch, sllm, reps=5):
+    """K4 (checksum) and K3 (scatter + checksum) on the device-resident partition image
+    (the real partition bytes, copied to HBM once; >= 1 GiB), HBM roofline.
+    K4: CUDA events around the call on the launching stream (the call is asynchronous).
+    K3: CUDA events the library records around the launch itself (the call also uploads
+    the segment and checksum tables and reads the result word, which are not the kernel).
+    Best of `reps`."""
+    p = sorted(bufs)[0]
     L = idx.partitions[p].length
     n = min(L, 4 << 30) // (1 << 20) * (1 << 20)
+    if 2 * L + (1 << 30) > torch.cuda.mem_get_info()[0]:  # image + per-tensor buffers must fit
+        return None
     src = torch.empty(L, dtype=torch.uint8, device="cuda")
-    src.random_(0, 256)
+    src.copy_(bufs[p].torch())
     out = torch.empty(-(-n // (1 << 20)), dtype=torch.int64, device="cuda")
     st = torch.cuda.current_stream()
     res = {}
@@ -259,24 +266,16 @@ def standalone_hbm(idx, torch, sllm, reps=5):
         b.synchronize()
         ts.append(a.elapsed_time(b))
     t = min(ts) * 1e-3
-    res["k4"] = {"bytes": n, "ms": t * 1e3, "GBps": n / t / 1e9}
+    table = idx.block_checksums(p)[:out.numel()]
+    res["k4"] = {"bytes": n, "ms": t * 1e3, "GBps": n / t / 1e9,
+                 "checksums_equal_index": bool((out.cpu().numpy().view("uint64") == table).all())}
     # K3: scatter the whole partition image into per-tensor buffers (read L + write payload)
-    _, per = sllm.allocate(idx, {0: 0}, scatter=True)
-    ts = []
-    ok = True
-    for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        try:
-            sllm.materialise_device(idx, p, src.data_ptr(), per, 0, st)
-        except sllm.SllmError as ex:  # random image: checksums cannot match, bytes still move
-            ok = ex.status == 9
-        b.record()
-        b.synchronize()
-        ts.append(a.elapsed_time(b))
+    _, per = sllm.allocate(idx, {p: 0}, scatter=True, partitions=[p])
+    ts = [sllm.materialise_device(idx, p, src.data_ptr(), per, 0, st, timed=True) for _ in range(reps)]
     t = min(ts) * 1e-3
-    payload = idx.info()["payload_bytes"]
-    res["k3"] = {"bytes": L + payload, "ms": t * 1e3, "GBps": (L + payload) / t / 1e9, "status_ok": ok}
+    payload = sum(x.nbytes for x in idx.tensors if x.partition == p)
+    res["k3"] = {"bytes": L + payload, "ms": t * 1e3, "GBps": (L + payload) / t / 1e9, "status_ok": True,
+                 "timing": "library CUDA events around the K3 launch"}
     del per, src, out
     torch.cuda.empty_cache()
     return res
@@ -350,7 +349,7 @@ def main():
         else:
             sig = torch.zeros(2, dtype=torch.int32, device=dev)
             comm = sllm.Comm.peers(1, 0, gpu, [bases[0].data_ptr()], [sig.data_ptr()], keep=[sig])
-    elif args.fanout == "bcast":  # NCCL communicator over the process group
+    elif args.fanout in ("bcast", "allgather"):  # NCCL communicator over the process group
         comm = sllm.Comm.from_process_group(gpu) if world > 1 else sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, gpu)
 
     def step(prof: bool):
@@ -459,7 +458,8 @@ def main():
     if not args.no_standalone and rank == 0:
         bases = per_tensor = None
         torch.cuda.empty_cache()
-        standalone = standalone_hbm(idx, torch, sllm)
+        standalone = standalone_hbm(idx, bufs, torch, sllm)
+    if standalone is not None:
         hbm = peaks().get("hbm_gbs", 6551.4)
         k4 = standalone["k4"]
         standalone["k4"]["frac_hbm"] = k4["GBps"] / hbm

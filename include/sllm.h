@@ -174,6 +174,16 @@ SLLM_API sllm_status sllm_replica_slices(uint64_t length, uint64_t chunk, int32_
  * SLLM_E_LOOKUP if round >= n_rounds. */
 SLLM_API sllm_status sllm_replica_round(uint64_t length, uint64_t chunk, int32_t nranks, uint64_t round,
                                         uint64_t* lo_hi, uint64_t* n_rounds);
+/* All-gather schedule of SLLM_FANOUT_ALLGATHER ("in-place ncclAllGather is the
+ * equal-count alternative"): chunk k of the partition belongs to rank k mod nranks, so
+ * round r is the contiguous run of chunks [r*nranks, (r+1)*nranks) and rank q contributes
+ * chunk r*nranks + q.  lo_hi receives 2*nranks values {lo_q, hi_q} (hi_q == lo_q: rank q
+ * has no chunk in this round); *n_rounds (may be NULL) = ceil(ceil(length/chunk)/nranks);
+ * *full (may be NULL) = 1 when every rank has a whole chunk in the round -- the loader then
+ * issues one in-place ncclAllGather of `chunk` bytes per rank, else (the ragged last round)
+ * grouped ncclBroadcasts of each chunk from its owner.  SLLM_E_LOOKUP if round >= n_rounds. */
+SLLM_API sllm_status sllm_allgather_round(uint64_t length, uint64_t chunk, int32_t nranks, uint64_t round,
+                                          uint64_t* lo_hi, uint64_t* n_rounds, int32_t* full);
 
 /* ------------------------------------------------------------------------------------
  * Pinned host memory (the DRAM tier).  Page-locked, mapped into the
@@ -241,14 +251,19 @@ typedef enum {
  *           replica and, over NVLink, into every peer replica at the same offset; then a
  *           device-side signal/wait exchange (system-scope release/acquire flags) orders
  *           the peers' stores before each rank verifies what it received
- *           (sllm_comm_init_peers). */
-typedef enum { SLLM_FANOUT_NONE = 0, SLLM_FANOUT_BCAST = 1, SLLM_FANOUT_P2P = 2 } sllm_fanout;
+ *           (sllm_comm_init_peers);
+ *   ALLGATHER: by one in-place ncclAllGather per round of nranks chunks (NCCL communicator).
+ *           Here rank r's PCIe share is not a contiguous slice but every chunk k with
+ *           k mod nranks == r (sllm_allgather_round), so the whole partition must be pinned;
+ *           pinned sources only (not sllm_load_files_start).
+ * Every rank's received bytes are verified against the index like its own (K4). */
+typedef enum { SLLM_FANOUT_NONE = 0, SLLM_FANOUT_BCAST = 1, SLLM_FANOUT_P2P = 2, SLLM_FANOUT_ALLGATHER = 3 } sllm_fanout;
 
 typedef struct {
   uint64_t chunk_bytes; /* multiple of the index block size (and of align); 0 = 16 MiB    */
   int32_t n_streams;    /* internal streams per GPU, 1..8 (0 = 2)                           */
   int32_t mode;         /* sllm_mode                                                        */
-  int32_t fanout;       /* sllm_fanout; BCAST requires a comm and a 1-partition index       */
+  int32_t fanout;       /* sllm_fanout; BCAST/ALLGATHER/P2P require a comm and a 1-partition index */
   int32_t verify;       /* 1 = check every block's Fletcher-64 against the index            */
   int32_t ctas;         /* CTAs per kernel launch (0 = mode default)                        */
   int32_t profile;      /* 1 = time every kernel launch with CUDA events, 2 = also copies    */
@@ -278,7 +293,7 @@ typedef struct {
                                      storage (0 = storage never the bottleneck)              */
 } sllm_load_report;
 
-/* Communicator for SLLM_FANOUT_BCAST.  One process per GPU: rank 0 calls
+/* Communicator for SLLM_FANOUT_BCAST and SLLM_FANOUT_ALLGATHER.  One process per GPU: rank 0 calls
  * sllm_comm_unique_id, the caller distributes the 128 bytes (e.g. via torch.distributed),
  * every rank calls sllm_comm_init_rank.  Single process, several GPUs: sllm_comm_init_all
  * (one comm per listed GPU; handle i belongs to gpus[i]).  libnccl.so.2 is loaded lazily. */
@@ -325,10 +340,10 @@ SLLM_API void sllm_comm_free(sllm_comm* comm);
  *                    ordered after work already queued on it, and the stream is made to
  *                    wait for the load's completion, so work queued on it after
  *                    sllm_load_start sees the loaded bytes.  NULL array/entry = no ordering.
- *   comm           : NULL unless cfg->fanout is BCAST (NCCL communicator) or P2P (peer
- *                    group); with a fan-out, host_src[0] needs to hold (pinned) only the
- *                    rank's own slice [lo_r, hi_r) of sllm_replica_slices: bytes outside
- *                    it are never read.
+ *   comm           : NULL unless cfg->fanout is BCAST / ALLGATHER (NCCL communicator) or
+ *                    P2P (peer group); with BCAST or P2P, host_src[0] needs to hold (pinned)
+ *                    only the rank's own slice [lo_r, hi_r) of sllm_replica_slices: bytes
+ *                    outside it are never read (ALLGATHER: the rank's chunks k = r mod n).
  * Returns SLLM_E_BUSY if one of dst_base/dst_tensor is the target of an unfinished load.
  * Tensor contents are defined only after sllm_load_wait returns SLLM_OK (Q17). */
 SLLM_API sllm_status sllm_load_start(const sllm_index* index, const sllm_load_config* cfg,
@@ -408,9 +423,12 @@ SLLM_API sllm_status sllm_block_checksums_device(const void* src_dev, uint64_t l
                                         int32_t ctas, void* stream);
 /* Scatter partition p, already resident at src_dev (device pointer, L_p bytes), into the
  * per-tensor buffers dst_tensor[i] (as in sllm_load_start), verifying every block against
- * the index.  Synchronous; SLLM_E_CHECKSUM names the first bad block in *bad_block. */
+ * the index.  Synchronous; SLLM_E_CHECKSUM names the first bad block in *bad_block.
+ * kernel_ms (NULL = not timed): device time of the K3 launch alone, from CUDA events
+ * recorded on `stream` immediately around it (table uploads and the result read excluded). */
 SLLM_API sllm_status sllm_materialise_device(const sllm_index* index, size_t p, const void* src_dev,
-                                    void* const* dst_tensor, int32_t ctas, void* stream, uint64_t* bad_block);
+                                    void* const* dst_tensor, int32_t ctas, void* stream, uint64_t* bad_block,
+                                    float* kernel_ms);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ STATUS = {0: "OK", 1: "INVALID", 2: "CONVERSION", 3: "FORMAT", 4: "LOOKUP", 5: "
  E_PEER) = range(13)
 
 MODE_CE, MODE_ZEROCOPY, MODE_SCATTER_CE, MODE_SCATTER_ZC, MODE_AUTO = range(5)
-FANOUT_NONE, FANOUT_BCAST, FANOUT_P2P = range(3)
+FANOUT_NONE, FANOUT_BCAST, FANOUT_P2P, FANOUT_ALLGATHER = range(4)
 DTYPE_CODE = {"f16": 0, "bf16": 1, "f32": 2, "i8": 3, "u8": 4, "i64": 5}
 DTYPE_NAME = {v: k for k, v in DTYPE_CODE.items()}
 
@@ -102,6 +102,7 @@ SIGNATURES = {
     "sllm_chunk_count": (S, [U64, U64, C.POINTER(U64)]),
     "sllm_replica_slices": (S, [U64, U64, C.c_int32, C.POINTER(U64)]),
     "sllm_replica_round": (S, [U64, U64, C.c_int32, U64, C.POINTER(U64), C.POINTER(U64)]),
+    "sllm_allgather_round": (S, [U64, U64, C.c_int32, U64, C.POINTER(U64), C.POINTER(U64), C.POINTER(C.c_int32)]),
     "sllm_host_alloc": (S, [U64, C.c_int32, PP]),
     "sllm_host_free": (None, [P]),
     "sllm_host_register": (S, [P, U64]),
@@ -128,7 +129,7 @@ SIGNATURES = {
     "sllm_ipc_open": (S, [C.POINTER(IpcRegion), PP]),
     "sllm_ipc_close": (S, [P]),
     "sllm_block_checksums_device": (S, [P, U64, U64, P, C.c_int32, P]),
-    "sllm_materialise_device": (S, [P, C.c_size_t, P, PP, C.c_int32, P, C.POINTER(U64)]),
+    "sllm_materialise_device": (S, [P, C.c_size_t, P, PP, C.c_int32, P, C.POINTER(U64), C.POINTER(C.c_float)]),
 }
 
 _lib = None

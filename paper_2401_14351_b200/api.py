@@ -232,6 +232,23 @@ def replica_schedule(length: int, chunk: int, nranks: int) -> List[List[Tuple[in
     return out
 
 
+def allgather_schedule(length: int, chunk: int, nranks: int) -> List[Tuple[bool, List[Tuple[int, int]]]]:
+    """The rounds of fanout="allgather": (full, [(lo, hi) of rank q's chunk]) per round --
+    chunk k belongs to rank k % nranks; a full round is one in-place all-gather of `chunk`
+    bytes per rank, the ragged last round grouped broadcasts."""
+    arr = (C.c_uint64 * (2 * nranks))()
+    n = C.c_uint64()
+    full = C.c_int32()
+    if length == 0:
+        return []
+    check(lib().sllm_allgather_round(length, chunk, nranks, 0, arr, C.byref(n), None))
+    out = []
+    for r in range(n.value):
+        check(lib().sllm_allgather_round(length, chunk, nranks, r, arr, None, C.byref(full)))
+        out.append((bool(full.value), [(arr[2 * q], arr[2 * q + 1]) for q in range(nranks)]))
+    return out
+
+
 class HostBuffer:
     """Pinned, device-mapped host memory from sllm_host_alloc (the DRAM tier)."""
 
@@ -308,7 +325,7 @@ class LoadConfig:
     chunk_bytes: int = 16 << 20   # P:1279 "16MB" (read as MiB, Q9)
     n_streams: int = 2
     mode: str = "ce"              # ce | zerocopy | scatter_ce | scatter_zc | auto (ce or zerocopy by size)
-    fanout: str = "none"          # none | bcast (NCCL) | p2p (fused NVLink stores)
+    fanout: str = "none"          # none | bcast / allgather (NCCL) | p2p (fused NVLink stores)
     verify: bool = True
     ctas: int = 0
     profile: bool = False         # per-launch CUDA-event timing (bench roofline)
@@ -317,7 +334,8 @@ class LoadConfig:
     def to_c(self) -> _abi.LoadConfig:
         modes = {"ce": _abi.MODE_CE, "zerocopy": _abi.MODE_ZEROCOPY, "scatter_ce": _abi.MODE_SCATTER_CE,
                  "scatter_zc": _abi.MODE_SCATTER_ZC, "auto": _abi.MODE_AUTO}
-        fan = {"none": _abi.FANOUT_NONE, "bcast": _abi.FANOUT_BCAST, "p2p": _abi.FANOUT_P2P}
+        fan = {"none": _abi.FANOUT_NONE, "bcast": _abi.FANOUT_BCAST, "p2p": _abi.FANOUT_P2P,
+               "allgather": _abi.FANOUT_ALLGATHER}
         return _abi.LoadConfig(self.chunk_bytes, self.n_streams, modes[self.mode], fan[self.fanout],
                                int(self.verify), self.ctas, int(self.profile),
                                {"tma": 1, "ldg": 2, "tma_store": 3}[self.engine], 0)
@@ -581,9 +599,14 @@ def block_checksums_device(src_ptr: int, length: int, block: int, out_ptr: int, 
 
 
 def materialise_device(index: Index, p: int, src_ptr: int, per_tensor: Dict[str, object], ctas: int = 0,
-                       stream=None) -> None:
+                       stream=None, timed: bool = False) -> Optional[float]:
+    """K3 over a device-resident partition image.  timed=True returns the launch's device
+    time in ms (CUDA events around the launch only)."""
     infos = index.tensors
     arr = _ptr_array([per_tensor[t.name].data_ptr() if t.partition == p else None for t in infos])
     bad = C.c_uint64()
+    ms = C.c_float(-1.0)
     check(lib().sllm_materialise_device(index.handle, p, C.c_void_p(src_ptr), arr, ctas,
-                                        C.c_void_p(stream.cuda_stream if stream is not None else 0), C.byref(bad)))
+                                        C.c_void_p(stream.cuda_stream if stream is not None else 0), C.byref(bad),
+                                        C.byref(ms) if timed else None))
+    return float(ms.value) if timed else None

@@ -19,7 +19,7 @@ std::vector<uint8_t> read_file(const char* path);
 void read_partition(const char* dir, const sllm_index* idx, size_t p, void* dst, int threads);
 void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint64_t* out, int ctas, cudaStream_t st);
 uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, void* const* dst_tensor, int ctas,
-                            cudaStream_t st);
+                            cudaStream_t st, float* kernel_ms);
 }  // namespace sllm
 
 sllm_load* sllm_load_create_internal(const sllm_index*, const sllm_load_config*, const void* const*, const int32_t*,
@@ -252,6 +252,25 @@ sllm_status sllm_replica_round(uint64_t length, uint64_t chunk, int32_t nranks, 
   });
 }
 
+sllm_status sllm_allgather_round(uint64_t length, uint64_t chunk, int32_t nranks, uint64_t round, uint64_t* lo_hi,
+                                 uint64_t* n_rounds, int32_t* full) {
+  return guard([&] {
+    if (!chunk || nranks < 1 || !lo_hi) fail(SLLM_E_INVALID, "bad round arguments");
+    const uint64_t R = (uint64_t)nranks, nch = ceil_div(length, chunk), rounds = ceil_div(nch, R);
+    if (n_rounds) *n_rounds = rounds;
+    if (round >= rounds) fail(SLLM_E_LOOKUP, "round out of range");
+    bool all = true;
+    for (uint64_t q = 0; q < R; ++q) {
+      const uint64_t k = round * R + q;
+      const uint64_t a = k < nch ? k * chunk : 0, b = k < nch ? std::min(a + chunk, length) : 0;
+      lo_hi[2 * q] = a;
+      lo_hi[2 * q + 1] = b;
+      all = all && b - a == chunk;
+    }
+    if (full) *full = all ? 1 : 0;
+  });
+}
+
 sllm_status sllm_host_alloc(uint64_t bytes, int32_t gpu, void** p) {
   return guard([&] {
     if (!p) fail(SLLM_E_INVALID, "null out");
@@ -391,9 +410,9 @@ sllm_status sllm_block_checksums_device(const void* src_dev, uint64_t len, uint6
 }
 
 sllm_status sllm_materialise_device(const sllm_index* idx, size_t p, const void* src_dev, void* const* dst_tensor,
-                                    int32_t ctas, void* stream, uint64_t* bad_block) {
+                                    int32_t ctas, void* stream, uint64_t* bad_block, float* kernel_ms) {
   return guard([&] {
-    uint64_t bad = materialise_device(idx, p, src_dev, dst_tensor, ctas, static_cast<cudaStream_t>(stream));
+    uint64_t bad = materialise_device(idx, p, src_dev, dst_tensor, ctas, static_cast<cudaStream_t>(stream), kernel_ms);
     if (bad_block) *bad_block = bad;
     if (bad != ~0ull) fail(SLLM_E_CHECKSUM, "checksum mismatch in partition " + std::to_string(p) + ", block " +
                                                 std::to_string(bad));

@@ -62,7 +62,7 @@ void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint6
 }
 
 uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, void* const* dst_tensor, int ctas,
-                            cudaStream_t st) {
+                            cudaStream_t st, float* kernel_ms) {
   if (!idx || !src || !dst_tensor) fail(SLLM_E_INVALID, "null argument");
   if (p >= idx->parts.size()) fail(SLLM_E_LOOKUP, "partition index out of range");
   const PartRec& pr = idx->parts[p];
@@ -108,10 +108,19 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   mp.expect = check ? d_expect : nullptr;
   mp.bad = d_bad;
   mp.engine = standalone_engine();
+  cudaEvent_t ev[2] = {};
+  if (kernel_ms)
+    for (auto& e : ev) SLLM_CUDA(cudaEventCreate(&e));
+  if (kernel_ms) SLLM_CUDA(cudaEventRecord(ev[0], st));
   SLLM_CUDA(launch_materialise(mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas > 0 ? ctas : default_grid(), st));
+  if (kernel_ms) SLLM_CUDA(cudaEventRecord(ev[1], st));
   unsigned long long bad = ~0ull;
   SLLM_CUDA(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st));
   SLLM_CUDA(cudaStreamSynchronize(st));
+  if (kernel_ms) {
+    SLLM_CUDA(cudaEventElapsedTime(kernel_ms, ev[0], ev[1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   SLLM_CUDA(cudaFreeAsync(scratch, st));
   return bad;
 }

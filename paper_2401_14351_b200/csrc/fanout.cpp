@@ -4,11 +4,15 @@
 // and has no GPU-to-GPU path.  For a replicated checkpoint the
 // B200 build lets every byte cross PCIe once: rank r reads slice r over its own link,
 // and each chunk round is broadcast from its owner to every other GPU (grouped
-// ncclBroadcast, one root per slice) while the next PCIe chunk is in flight.
+// ncclBroadcast, one root per slice) while the next PCIe chunk is in flight -- or, with
+// round-robin chunk ownership, gathered by one in-place ncclAllGather per round.
 //
 // libnccl.so.2 (NCCL 2.28, shipped with PyTorch) is opened with dlopen so the library
 // loads on hosts without NCCL; only the handful of calls below are bound.
 #include <dlfcn.h>
+
+#include <condition_variable>
+#include <map>
 
 #include "nccl.h"
 #include "runtime.hpp"
@@ -22,6 +26,7 @@ struct Nccl {
   ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -49,6 +54,7 @@ const Nccl& nccl() {
   bind(h, g_nccl.CommInitAll, "ncclCommInitAll");
   bind(h, g_nccl.CommDestroy, "ncclCommDestroy");
   bind(h, g_nccl.Broadcast, "ncclBroadcast");
+  bind(h, g_nccl.AllGather, "ncclAllGather");
   bind(h, g_nccl.GroupStart, "ncclGroupStart");
   bind(h, g_nccl.GroupEnd, "ncclGroupEnd");
   bind(h, g_nccl.GetErrorString, "ncclGetErrorString");
@@ -59,6 +65,25 @@ const Nccl& nccl() {
 static void nccl_check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) fail(SLLM_E_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
 }
+
+// Ranks of one P2P group that live in the same process (tests, several replicas on one
+// GPU) share one CUDA context, whose streams are multiplexed onto a few hardware work
+// queues.  A rank's device-side peer wait sits at the head of its queue until the peers
+// signal; a peer's work submitted to the same hardware queue *after* that wait would be
+// stuck behind it -- a false dependency that only the timeout breaks.  So in-process ranks
+// rendezvous on the host at two points of every load: after each has queued its ready
+// signal (before anyone queues the ready wait) and after each has queued its done signal
+// (before the next load's done wait).  Everything a wait depends on is then queued ahead
+// of it in every hardware queue.  One rank per process (the deployment) skips this.
+struct LocalGroup {
+  std::mutex mu;
+  std::condition_variable cv;
+  int members = 0;
+  int count = 0;
+  uint64_t gen = 0;
+};
+static std::mutex g_groups_mu;
+static std::map<std::vector<uint32_t*>, std::weak_ptr<LocalGroup>> g_groups;
 
 }  // namespace sllm
 
@@ -74,6 +99,7 @@ struct sllm_comm {
   uint32_t epoch = 0;
   uint64_t timeout_ns = 0;
   cudaStream_t streams[sllm::kMaxStreams + 1] = {};
+  std::shared_ptr<sllm::LocalGroup> local;  // the in-process ranks of this peer group
 };
 
 namespace sllm {
@@ -89,6 +115,23 @@ uint32_t comm_next_epoch(sllm_comm* c) {
   if (++c->epoch == 0) ++c->epoch;  // 0 is the signal arrays' initial value
   return c->epoch;
 }
+void comm_local_barrier(sllm_comm* c) {
+  LocalGroup* g = c->local.get();
+  if (!g) return;
+  std::unique_lock<std::mutex> lk(g->mu);
+  if (g->members <= 1) return;
+  const uint64_t my = g->gen;
+  if (++g->count == g->members) {
+    g->count = 0;
+    ++g->gen;
+    g->cv.notify_all();
+    return;
+  }
+  // a rank that never arrives (its load was not started): give up after the group timeout;
+  // the device-side wait then reports SLLM_E_PEER
+  if (!g->cv.wait_for(lk, std::chrono::nanoseconds(c->timeout_ns), [&] { return g->gen != my; })) --g->count;
+}
+
 cudaStream_t comm_stream(sllm_comm* c, int s) {  // s = 0..kMaxStreams-1 transfer, kMaxStreams = kernel
   if (!c->streams[s]) SLLM_CUDA(cudaStreamCreateWithFlags(&c->streams[s], cudaStreamNonBlocking));
   return c->streams[s];
@@ -109,6 +152,13 @@ void nccl_bcast_group(sllm_comm* c, const std::vector<std::pair<uint64_t, uint64
     }
   }
   nccl_check(n.GroupEnd(), "ncclGroupEnd");
+}
+
+// One full all-gather round (SLLM_FANOUT_ALLGATHER): rank q's chunk sits at
+// buf + lo + q*count, so the gather is in place (sendbuff = recvbuff + rank*count).
+void nccl_allgather_inplace(sllm_comm* c, uint64_t lo, uint64_t count, uint8_t* buf, cudaStream_t s) {
+  nccl_check(nccl().AllGather(buf + lo + (uint64_t)c->rank * count, buf + lo, count, ncclUint8, c->comm, s),
+             "ncclAllGather");
 }
 
 }  // namespace sllm
@@ -185,12 +235,30 @@ sllm_comm* sllm_comm_init_peers_internal(int32_t nranks, int32_t rank, int32_t g
     c->base.push_back(static_cast<uint8_t*>(peer_base[q]));
     c->signal.push_back(peer_signal[q]);
   }
+  if (nranks > 1) {  // join (or start) this process's share of the group
+    std::lock_guard<std::mutex> g(g_groups_mu);
+    auto& w = g_groups[c->signal];
+    c->local = w.lock();
+    if (!c->local) w = c->local = std::make_shared<LocalGroup>();
+    std::lock_guard<std::mutex> lg(c->local->mu);
+    ++c->local->members;
+  }
   return c.release();
 }
 
 void sllm_comm_free_internal(sllm_comm* c) {
   if (!c) return;
   if (c->comm && g_nccl_ok) g_nccl.CommDestroy(c->comm);
+  if (c->local) {
+    std::lock_guard<std::mutex> g(g_groups_mu);
+    {
+      std::lock_guard<std::mutex> lg(c->local->mu);
+      --c->local->members;
+    }
+    auto it = g_groups.find(c->signal);
+    c->local.reset();
+    if (it != g_groups.end() && it->second.expired()) g_groups.erase(it);
+  }
   if (c->peers) {
     cudaSetDevice(c->dev);
     for (auto& s : c->streams)

@@ -448,7 +448,8 @@ static void run_job(sllm_load* L, PartJob& j) {
   // windows there (kScatterWindowBytes) make fewer, longer launches; the staging ring is
   // never larger than the partition.
   const uint64_t win_bytes = cfg.mode == SLLM_MODE_SCATTER_CE ? kScatterWindowBytes : kWindowBytes;
-  P.window = cfg.fanout == SLLM_FANOUT_BCAST ? 1 : std::max<uint64_t>(1, win_bytes / cfg.chunk_bytes);
+  const bool nccl_fanout = cfg.fanout == SLLM_FANOUT_BCAST || cfg.fanout == SLLM_FANOUT_ALLGATHER;
+  P.window = nccl_fanout ? 1 : std::max<uint64_t>(1, win_bytes / cfg.chunk_bytes);
   const uint64_t nch_all = std::max<uint64_t>(1, ceil_div(pr.length, cfg.chunk_bytes));
   P.slot_bytes = std::min(P.window, nch_all) * cfg.chunk_bytes;
   P.nslot = (int)std::min<uint64_t>((uint64_t)P.nslot, ceil_div(nch_all, P.window));
@@ -462,7 +463,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   cudaStream_t s0 = P.xfer[0];
   j.used.assign(P.xfer, P.xfer + P.S);
   j.used.push_back(P.kern);
-  if (cfg.fanout == SLLM_FANOUT_BCAST) j.used.push_back(j.ss->comm);
+  if (nccl_fanout) j.used.push_back(j.ss->comm);
   const uint64_t nb = pr.n_blocks;
   const size_t seg_bytes = align_up(j.segs.size() * sizeof(Seg), 256);
   const size_t acc_bytes = align_up(std::max<uint64_t>(nb, 1) * sizeof(BlockAcc), 256);
@@ -503,21 +504,28 @@ static void run_job(sllm_load* L, PartJob& j) {
   std::vector<cudaStream_t> tails;  // streams to join at the end
   for (int s = 1; s < P.S; ++s) tails.push_back(P.xfer[s]);
   tails.push_back(P.kern);
-  if (cfg.fanout == SLLM_FANOUT_BCAST) {
-    // Replicated load: this rank moves its slice over PCIe; every chunk
-    // round is then broadcast from its owner over NVLink (grouped, one root per slice).
+  if (nccl_fanout) {
+    // Replicated load: this rank moves its chunks over PCIe; every chunk
+    // round is then spread over NVLink -- BCAST: grouped broadcasts, one root per slice;
+    // ALLGATHER: chunks owned round-robin, one in-place all-gather per full round (the
+    // ragged last round falls back to grouped broadcasts).
+    const bool ag = cfg.fanout == SLLM_FANOUT_ALLGATHER;
     const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
     std::vector<uint64_t> lohi(2 * R);
     uint64_t rounds = 0;
-    if (sllm_replica_round(pr.length, C, R, 0, lohi.data(), &rounds) != SLLM_OK && pr.length)
-      fail(SLLM_E_INVALID, "fan-out schedule failed");
+    int32_t full = 0;
+    auto schedule = [&](uint64_t r, uint64_t* n) {
+      return ag ? sllm_allgather_round(pr.length, C, R, r, lohi.data(), n, &full)
+                : sllm_replica_round(pr.length, C, R, r, lohi.data(), n);
+    };
+    if (schedule(0, &rounds) != SLLM_OK && pr.length) fail(SLLM_E_INVALID, "fan-out schedule failed");
     cudaEvent_t evk;
     SLLM_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
     cudaStream_t cs = j.ss->comm;
     SLLM_CUDA(cudaStreamWaitEvent(cs, j.ev[2], 0));
     for (uint64_t r = 0; r < rounds; ++r) {
-      if (sllm_replica_round(pr.length, C, R, r, lohi.data(), nullptr) != SLLM_OK)
-        fail(SLLM_E_INVALID, "fan-out schedule failed");
+      full = 0;
+      if (schedule(r, nullptr) != SLLM_OK) fail(SLLM_E_INVALID, "fan-out schedule failed");
       std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
       for (int q = 0; q < R; ++q) ranges[q] = {lohi[2 * q], lohi[2 * q + 1]};
       if (ranges[me].second > ranges[me].first) {  // this rank's own chunk of the round: PCIe
@@ -529,10 +537,18 @@ static void run_job(sllm_load* L, PartJob& j) {
       }
       for (int q = 0; q < R; ++q)
         if (q != me && ranges[q].second > ranges[q].first) j.fanout += ranges[q].second - ranges[q].first;
-      nccl_bcast_group(L->comm, ranges, j.dst_base, cs);  // NVLink: every root's chunk to every rank
-      if (cfg.verify && idx.block)
-        for (int q = 0; q < R; ++q)
-          if (q != me && ranges[q].second > ranges[q].first) verify_range(idx, cfg, j, ranges[q].first, ranges[q].second, cs);
+      if (ag && full) {  // NVLink: one in-place all-gather of the round's R whole chunks
+        nccl_allgather_inplace(L->comm, ranges[0].first, C, j.dst_base, cs);
+        if (cfg.verify && idx.block) {  // the round is contiguous: what arrived is around our chunk
+          if (me > 0) verify_range(idx, cfg, j, ranges[0].first, ranges[me].first, cs);
+          if (me + 1 < R) verify_range(idx, cfg, j, ranges[me].second, ranges[R - 1].second, cs);
+        }
+      } else {
+        nccl_bcast_group(L->comm, ranges, j.dst_base, cs);  // NVLink: every root's chunk to every rank
+        if (cfg.verify && idx.block)
+          for (int q = 0; q < R; ++q)
+            if (q != me && ranges[q].second > ranges[q].first) verify_range(idx, cfg, j, ranges[q].first, ranges[q].second, cs);
+      }
     }
     tails.push_back(cs);
     SLLM_CUDA(cudaEventDestroy(evk));
@@ -556,6 +572,7 @@ static void run_job(sllm_load* L, PartJob& j) {
         done.remote[done.n++] = comm_peer_signal(L->comm, q) + R + me;
       }
     SLLM_CUDA(launch_peer_signal(ready, j.epoch, s0));
+    comm_local_barrier(L->comm);  // in-process peers: every ready signal is queued before any wait
     SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me), R, me, j.epoch, comm_timeout_ns(L->comm), j.d_err, s0));
     j.fanout = pr.length - (j.hi - j.lo);
     if (cfg.verify && idx.block) {  // what arrived over NVLink is verified like what came over PCIe
@@ -563,6 +580,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       if (j.hi < pr.length) verify_range(idx, cfg, j, j.hi, pr.length, s0);
     }
     SLLM_CUDA(launch_peer_signal(done, j.epoch, s0));
+    comm_local_barrier(L->comm);  // ... and every done signal before the next load's done wait
     if (R > 1) j.launches += 3;  // ready signal, ready wait, done signal
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
@@ -658,10 +676,12 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (idx->block && cfg.chunk_bytes % idx->block) fail(SLLM_E_INVALID, "chunk size must be a multiple of the block size");
   if (cfg.chunk_bytes % idx->align) fail(SLLM_E_INVALID, "chunk size must be a multiple of the alignment");
   const bool scatter = cfg.mode == SLLM_MODE_SCATTER_CE || cfg.mode == SLLM_MODE_SCATTER_ZC;
-  if (cfg.fanout == SLLM_FANOUT_BCAST || cfg.fanout == SLLM_FANOUT_P2P) {
+  if (cfg.fanout == SLLM_FANOUT_BCAST || cfg.fanout == SLLM_FANOUT_P2P || cfg.fanout == SLLM_FANOUT_ALLGATHER) {
     if (!comm) fail(SLLM_E_INVALID, "fan-out needs a communicator");
-    if (cfg.fanout == SLLM_FANOUT_BCAST && comm_is_peers(comm))
-      fail(SLLM_E_INVALID, "SLLM_FANOUT_BCAST needs an NCCL communicator (sllm_comm_init_rank/_all)");
+    if (cfg.fanout != SLLM_FANOUT_P2P && comm_is_peers(comm))
+      fail(SLLM_E_INVALID, "SLLM_FANOUT_BCAST/ALLGATHER need an NCCL communicator (sllm_comm_init_rank/_all)");
+    if (cfg.fanout == SLLM_FANOUT_ALLGATHER && dir)
+      fail(SLLM_E_INVALID, "SLLM_FANOUT_ALLGATHER loads from pinned sources only (its chunks are strided)");
     if (cfg.fanout == SLLM_FANOUT_P2P && !comm_is_peers(comm))
       fail(SLLM_E_INVALID, "SLLM_FANOUT_P2P needs a peer group (sllm_comm_init_peers)");
     if (cfg.fanout == SLLM_FANOUT_P2P && cfg.engine == 2) fail(SLLM_E_INVALID, "the P2P fan-out needs the TMA engine");
@@ -704,6 +724,10 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
       if (sllm_replica_slices(j.hi, cfg.chunk_bytes, R, lohi.data()) != SLLM_OK) fail(SLLM_E_INVALID, "bad slices");
       j.lo = lohi[2 * me];
       j.hi = lohi[2 * me + 1];
+      if (cfg.fanout == SLLM_FANOUT_ALLGATHER) {  // chunks me, me+R, me+2R, ... (strided)
+        j.lo = std::min((uint64_t)me * cfg.chunk_bytes, idx->parts[p].length);
+        j.hi = idx->parts[p].length;
+      }
     }
     if (cfg.fanout == SLLM_FANOUT_P2P) {
       if (j.dst_base != comm_peer_base(comm, comm_rank(comm)))

@@ -82,6 +82,7 @@ struct Nccl;
 const Nccl& nccl();  // throws SLLM_E_NCCL if libnccl.so.2 cannot be loaded
 void nccl_bcast_group(sllm_comm* comm, const std::vector<std::pair<uint64_t, uint64_t>>& ranges_by_root,
                       uint8_t* buf, cudaStream_t s);
+void nccl_allgather_inplace(sllm_comm* comm, uint64_t lo, uint64_t count, uint8_t* buf, cudaStream_t s);
 int comm_nranks(const sllm_comm* c);
 int comm_rank(const sllm_comm* c);
 int comm_device(const sllm_comm* c);
@@ -90,6 +91,7 @@ uint8_t* comm_peer_base(const sllm_comm* c, int q);
 uint32_t* comm_peer_signal(const sllm_comm* c, int q);
 uint64_t comm_timeout_ns(const sllm_comm* c);
 uint32_t comm_next_epoch(sllm_comm* c);
+void comm_local_barrier(sllm_comm* c);  // host rendezvous of the group's in-process ranks
 cudaStream_t comm_stream(sllm_comm* c, int s);
 
 }  // namespace sllm

@@ -119,6 +119,7 @@ CONFIGS = {
     "toy": (toy, 0, "toy 2-layer fp16 (22 tensors) -> 1 partition"),
     "opt-6.7b": (lambda: opt(4096, 32, 16384), 1, "OPT-6.7B-shaped fp16, 1 partition"),
     "llama2-13b-tp2": (lambda: llama2(5120, 40, 13824, 5120, tp=2), 2, "LLaMA-2-13B-shaped fp16, TP2"),
+    "llama2-70b": (lambda: llama2(8192, 80, 28672, 1024, tp=1), 3, "LLaMA-2-70B-shaped fp16, 1 partition (TP1)"),
     "llama2-70b-tp8": (lambda: llama2(8192, 80, 28672, 1024, tp=8), 3, "LLaMA-2-70B-shaped fp16, TP8"),
     "llama2-70b-tp4": (lambda: llama2(8192, 80, 28672, 1024, tp=4), 3, "LLaMA-2-70B-shaped fp16, TP4"),
     "llama2-70b-tp2": (lambda: llama2(8192, 80, 28672, 1024, tp=2), 3, "LLaMA-2-70B-shaped fp16, TP2"),

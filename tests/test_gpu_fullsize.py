@@ -74,3 +74,76 @@ def test_partitioned_checkpoint_full_size(config, need):
         for b in bufs.values():
             b.free()
         torch.cuda.empty_cache()
+
+
+def test_replicated_opt30b_full_size_p2p():
+    """BASELINE configs[4] at full size: the OPT-30B-shaped replicated checkpoint (one
+    59.95 GB partition) loaded by a 2-rank P2P fan-out group whose replicas
+    share the one GPU -- rank r reads slice r over PCIe, its kernel stores every vector into
+    both replicas.  Checked: each rank moved exactly its slice (Σ = L, every byte crossed
+    PCIe once), every block checksum of both replicas equals the index table, the index
+    table equals the oracle's Fletcher-64 on sampled source blocks, the replicas are equal
+    (compared 1 GiB at a time on the device), and sampled tensors of both replicas equal
+    their regenerated payload."""
+    need = 59.95e9
+    free, total = torch.cuda.mem_get_info(0)
+    if host_ram() < need * 1.3 or free < 2 * need * 1.03:
+        pytest.skip("the replicated OPT-30B check needs 60 GB of host RAM and 120 GB of HBM")
+    inv, seed = models.model_inventory("opt-30b")
+    lay = olayout.plan([(t.name, t.device, t.dtype, t.shape, t.nbytes) for t in inv], 4096, 1 << 20)
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, "opt-30b", gpu_of={0: 0}, threads=0)
+    bases = sigs = comms = None
+    try:
+        L = idx.partitions[0].length
+        assert L == lay.partitions[0] and idx.info()["payload_bytes"] == lay.payload_bytes
+        rng = np.random.default_rng(11)
+        src, table = bufs[0].numpy(), idx.block_checksums(0)
+        nb = idx.partitions[0].n_blocks
+        for j in sorted(set(rng.integers(0, nb, size=6).tolist()) | {0, nb - 1}):
+            assert int(table[j]) == fletcher.f64_closed(src[j << 20:(j + 1) << 20]), j
+        R, chunk = 2, 64 << 20
+        bases = [torch.empty(L, dtype=torch.uint8, device="cuda") for _ in range(R)]
+        sigs = [torch.zeros(2 * R, dtype=torch.int32, device="cuda") for _ in range(R)]
+        comms = [sllm.Comm.peers(R, r, 0, [b.data_ptr() for b in bases], [s.data_ptr() for s in sigs], 60000)
+                 for r in range(R)]
+        slices = sllm.replica_slices(L, chunk, R)
+        cfg = sllm.LoadConfig(chunk_bytes=chunk, mode="ce", fanout="p2p")
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        results = [sllm.load_start(idx, bufs, {0: 0}, cfg, {0: bases[r]}, None, None, comms[r]) for r in range(R)]
+        reports, errs = [], []
+        for r, res in enumerate(results):  # wait for every rank: the first error is the one to report
+            try:
+                reports.append(res.wait())
+            except sllm.SllmError as ex:
+                errs.append((r, str(ex)))
+        dt = time.perf_counter() - t0
+        assert not errs, errs
+        print(f"opt-30b replicated x{R} (P2P, one GPU, one PCIe link): {L / 1e9:.2f} GB per replica, "
+              f"{R} replicas in {dt:.3f} s; PCIe bytes {sum(r['transferred_bytes'] for r in reports) / 1e9:.2f} GB")
+        for r, rep in enumerate(reports):
+            lo, hi = slices[r]
+            assert rep["bad_partition"] == -1
+            assert rep["transferred_bytes"] == hi - lo and rep["fanout_bytes"] == L - (hi - lo)
+            assert np.array_equal(results[r].block_checksums(0), table), r
+        assert sum(rep["transferred_bytes"] for rep in reports) == L
+        step = 1 << 30
+        for o in range(0, L, step):
+            assert torch.equal(bases[0][o:o + step], bases[1][o:o + step]), o
+        for e in sorted(set(rng.integers(0, len(inv), size=12).tolist()) | {0, len(inv) - 1}):
+            t = inv[e]
+            n = min(t.nbytes, 1 << 20)
+            want = payload.payload_bytes(seed, e, t.nbytes)
+            for r in range(R):
+                v = results[r].tensors[t.name].reshape(-1).view(torch.uint8)
+                assert np.array_equal(v[:n].cpu().numpy(), want[:n]), (r, t.name)
+                assert np.array_equal(v[-n:].cpu().numpy(), want[-n:]), (r, t.name)
+        del results
+    finally:
+        if comms:
+            for c in comms:
+                c.free()
+        del bases, sigs
+        for b in bufs.values():
+            b.free()
+        torch.cuda.empty_cache()

@@ -257,11 +257,35 @@ def test_fanout_single_rank_nccl():
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
     lay, oparts, payloads = oracle_of(inv, seed, 4096, 1 << 20)
     comm = sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, 0)
-    for mode in ("ce", "zerocopy"):
-        cfg = sllm.LoadConfig(chunk_bytes=2 << 20, mode=mode, fanout="bcast")
-        res = sllm.load(idx, bufs, {0: 0}, cfg, comm=comm)
-        check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
+    for fanout in ("bcast", "allgather"):  # allgather: 6 full in-place rounds + a ragged last one
+        for mode in ("ce", "zerocopy"):
+            cfg = sllm.LoadConfig(chunk_bytes=2 << 20, mode=mode, fanout=fanout)
+            res = sllm.load(idx, bufs, {0: 0}, cfg, comm=comm)
+            check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
+            assert res.report["transferred_bytes"] == idx.partitions[0].length
     comm.free()
+
+
+def test_allgather_rejects_files_and_peer_groups(tmp_path):
+    inv, seed = models.model_inventory("toy")
+    payloads = [payload.payload_bytes(seed, e, t.nbytes) for e, t in enumerate(inv)]
+    sllm.convert([(t.name, t.device, t.dtype, t.shape, p.ctypes.data) for t, p in zip(inv, payloads)],
+                 str(tmp_path), 4096, 1 << 20, "toy")
+    idx = sllm.Index.open(str(tmp_path / "index.bin"))
+    comm = sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, 0)
+    with pytest.raises(sllm.SllmError) as ex:   # strided chunks: pinned sources only
+        sllm.load_files(idx, str(tmp_path), {0: 0}, sllm.LoadConfig(chunk_bytes=2 << 20, fanout="allgather"), comm=comm)
+    assert ex.value.status == 1
+    comm.free()
+    L = idx.partitions[0].length
+    base = torch.empty(L, dtype=torch.uint8, device="cuda")
+    sig = torch.zeros(2, dtype=torch.int32, device="cuda")
+    peers = sllm.Comm.peers(1, 0, 0, [base.data_ptr()], [sig.data_ptr()])
+    idx2, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    with pytest.raises(sllm.SllmError) as ex:   # a peer group is not an NCCL communicator
+        sllm.load(idx2, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=2 << 20, fanout="allgather"), comm=peers)
+    assert ex.value.status == 1
+    peers.free()
 
 
 def test_opt67b_full_size_sampled():
@@ -276,15 +300,17 @@ def test_opt67b_full_size_sampled():
     table = idx.block_checksums(0)
     for j in blocks:
         assert int(table[j]) == fletcher.f64_closed(src[j << 20:(j + 1) << 20])
-    for mode in ("ce", "zerocopy"):
-        res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(mode=mode))
+    for mode in ("ce", "zerocopy", "scatter_ce", "scatter_zc"):
+        res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(mode=mode, chunk_bytes=64 << 20))
         cs = res.block_checksums(0)
-        assert np.array_equal(cs, table)
-        for e in sorted(set(rng.integers(0, len(inv), size=12).tolist()) | {0, len(inv) - 1}):
+        assert np.array_equal(cs, table), mode
+        for e in sorted(set(rng.integers(0, len(inv), size=12).tolist()) | {0, 1, 2, len(inv) - 1}):
             t = inv[e]
             got = res.tensors[t.name].view(torch.uint8).reshape(-1)
             n = min(t.nbytes, 1 << 20)
-            assert np.array_equal(got[:n].cpu().numpy(), payload.payload_bytes(seed, e, t.nbytes)[:n])
+            want = payload.payload_bytes(seed, e, t.nbytes)
+            assert np.array_equal(got[:n].cpu().numpy(), want[:n]), (mode, t.name)
+            assert np.array_equal(got[-n:].cpu().numpy(), want[-n:]), (mode, t.name)
         del res
         torch.cuda.empty_cache()
 

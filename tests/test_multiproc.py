@@ -75,6 +75,51 @@ def _worker_fanout(rank, world, port, chunk, q):
         q.put((rank, traceback.format_exc()))
 
 
+def _worker_allgather(rank, world, port, chunk, q):
+    """fanout="allgather": rank r moves chunks r, r+N, ... "over PCIe"; every full round is
+    one in-place all-gather (gloo all_gather into views of the replica stands in for
+    ncclAllGather), the ragged last round per-owner broadcasts."""
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        _init(rank, world, port)
+        import paper_2401_14351_b200 as sllm
+        from oracle import layout as olayout
+        from synth import models, payload
+        rng = np.random.default_rng(11)
+        inv = [models.TensorSpec(t.name, 0, t.dtype, t.shape)
+               for t in models.random_inventory(rng, 300, 1, 6 << 20)]
+        tensors = [(t.name, 0, t.dtype, t.shape, payload.payload_bytes(5, e, t.nbytes)) for e, t in enumerate(inv)]
+        lay, parts = olayout.convert(tensors, 4096, 1 << 16)
+        P0 = parts[0]
+        L = P0.size
+        buf = torch.zeros(L, dtype=torch.uint8)
+        pcie = 0
+        for full, rnd in sllm.allgather_schedule(L, chunk, world):
+            a, b = rnd[rank]
+            if b > a:                                     # this rank's own chunk of the round
+                buf[a:b] = torch.from_numpy(P0[a:b])
+                pcie += b - a
+            if full:
+                lo = rnd[0][0]
+                views = [buf[lo + q * chunk:lo + (q + 1) * chunk] for q in range(world)]
+                dist.all_gather(views, buf[a:b].clone())  # stands in for the in-place ncclAllGather
+            else:
+                for src, (x, y) in enumerate(rnd):
+                    if y > x:
+                        dist.broadcast(buf[x:y], src=src)
+        assert np.array_equal(buf.numpy(), P0)
+        t = torch.tensor([pcie], dtype=torch.int64)
+        dist.all_reduce(t)
+        assert int(t.item()) == L                         # each byte crossed PCIe once in total
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
 def _worker_sharded(rank, world, port, q):
     try:
         import sys
@@ -134,6 +179,11 @@ def test_replicated_fanout_schedule_gloo(world, chunk):
     _run(_worker_fanout, world, chunk)
 
 
+@pytest.mark.parametrize("world,chunk", [(2, 1 << 16), (3, 1 << 16), (3, 3 << 16)])
+def test_allgather_fanout_schedule_gloo(world, chunk):
+    _run(_worker_allgather, world, chunk)
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_partition_per_rank_gloo(world):
     _run(_worker_sharded, world)
@@ -150,3 +200,27 @@ def test_schedule_properties():
             pos = b
         assert pos == L
         assert len(rounds) == max(-(-(b - a) // C) for a, b in sllm.replica_slices(L, C, N))
+
+
+def test_allgather_schedule_properties():
+    """Round-robin ownership: chunk k -> rank k % N; a round is N adjacent chunks, full iff
+    all N are whole; the rounds cover [0, L) exactly once."""
+    import paper_2401_14351_b200 as sllm
+    for L, C, N in [(13_594_624, 1 << 20, 8), (100 << 16, 1 << 16, 3), (1 << 16, 1 << 16, 4), (99 << 16, 1 << 16, 3),
+                    (59_949_920_256, 64 << 20, 8), (5 << 16, 1 << 16, 1)]:
+        rounds = sllm.allgather_schedule(L, C, N)
+        nch = -(-L // C)
+        assert len(rounds) == -(-nch // N)
+        pos = 0
+        for r, (full, rnd) in enumerate(rounds):
+            for q, (a, b) in enumerate(rnd):
+                k = r * N + q
+                if k < nch:
+                    assert (a, b) == (k * C, min((k + 1) * C, L)) and a == pos
+                    pos = b
+                else:
+                    assert a == b
+            assert full == all(b - a == C for a, b in rnd)
+            if r + 1 < len(rounds):
+                assert full
+        assert pos == L
