@@ -84,10 +84,12 @@ def load_sample(index_blob: bytes, sources: Dict[int, object], byte_budget: int)
     B = layout.block or (1 << 20)
     for p, d in enumerate(layout.devices()):
         L = layout.partitions[d]
-        src = _u8(sources[d])
         hi = min(L, (max(byte_budget - done, 0) + B - 1) // B * B)
         if hi <= 0:
             break
+        if d not in sources:  # a partition this process does not hold (sharded runs)
+            continue
+        src = _u8(sources[d])
         dst = np.empty(hi, dtype=np.uint8)
         dst[:] = src[:hi]
         if layout.block:

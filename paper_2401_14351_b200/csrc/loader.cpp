@@ -13,6 +13,7 @@
 // proceeds on the other stream(s) -- the pipeline "avoids synchronization for all data
 // on each storage tier" without host round trips.
 #include <algorithm>
+#include <cstdlib>
 #include <set>
 
 #include "runtime.hpp"
@@ -233,6 +234,7 @@ struct Pipe {
   uint64_t slot_bytes = 0;                 // SCATTER_CE: one window of chunks
   uint64_t window = 1;                     // chunks per submission (kernel launch)
   uint64_t v_k0 = 0, v_k1 = 0;             // CE: landed chunks not yet verified [v_k0, v_k1)
+  std::vector<std::pair<uint64_t, uint64_t>> plan;  // SCATTER_CE from pinned DRAM: window chunk ranges
 };
 
 // sllm_load_config.engine -> MatParams.engine (0 LDG tiles, 1 TMA ring + STG, 2 TMA ring +
@@ -447,12 +449,33 @@ static void run_job(sllm_load* L, PartJob& j) {
   // SCATTER_CE stages whole windows in HBM and scatters each with one K3 launch: larger
   // windows there (kScatterWindowBytes) make fewer, longer launches; the staging ring is
   // never larger than the partition.
-  const uint64_t win_bytes = cfg.mode == SLLM_MODE_SCATTER_CE ? kScatterWindowBytes : kWindowBytes;
+  // (the file tier keeps kScatterFileWindowBytes: its windows are storage-ring slots)
+  const bool files = !j.file.empty();
+  uint64_t scatter_win = files ? kScatterFileWindowBytes : kScatterWindowBytes;
+  if (const char* e = getenv("SLLM_SCATTER_WINDOW_MIB"))  // measurement knob (A/B runs)
+    if (atoll(e) > 0 && !files) scatter_win = (uint64_t)atoll(e) << 20;
+  const uint64_t win_bytes = cfg.mode == SLLM_MODE_SCATTER_CE ? scatter_win : kWindowBytes;
   const bool nccl_fanout = cfg.fanout == SLLM_FANOUT_BCAST || cfg.fanout == SLLM_FANOUT_ALLGATHER;
   P.window = nccl_fanout ? 1 : std::max<uint64_t>(1, win_bytes / cfg.chunk_bytes);
   const uint64_t nch_all = std::max<uint64_t>(1, ceil_div(pr.length, cfg.chunk_bytes));
-  P.slot_bytes = std::min(P.window, nch_all) * cfg.chunk_bytes;
-  P.nslot = (int)std::min<uint64_t>((uint64_t)P.nslot, ceil_div(nch_all, P.window));
+  if (cfg.mode == SLLM_MODE_SCATTER_CE && !files) {
+    // windows of P.window chunks, halving over the last two windows' worth of chunks down
+    // to kScatterTailBytes, so the K3 that runs after the final copy is short
+    const uint64_t wmin = std::min<uint64_t>(P.window, std::max<uint64_t>(1, kScatterTailBytes / cfg.chunk_bytes));
+    uint64_t widest = 1;
+    for (uint64_t k0 = 0; k0 < nch_all;) {
+      const uint64_t rem = nch_all - k0;
+      const uint64_t n = std::min(rem, rem > 2 * P.window ? P.window : std::max(wmin, (rem + 1) / 2));
+      P.plan.emplace_back(k0, k0 + n);
+      widest = std::max(widest, n);
+      k0 += n;
+    }
+    P.slot_bytes = widest * cfg.chunk_bytes;
+    P.nslot = (int)std::min<uint64_t>((uint64_t)P.nslot, P.plan.size());
+  } else {
+    P.slot_bytes = std::min(P.window, nch_all) * cfg.chunk_bytes;
+    P.nslot = (int)std::min<uint64_t>((uint64_t)P.nslot, ceil_div(nch_all, P.window));
+  }
   if (!j.file.empty())  // (a replicated load reads only its slice [lo, hi) from storage)
     j.fsrc = file_source_open(j.file, j.lo, j.hi, P.window * cfg.chunk_bytes, j.io_threads, j.gpu);
   SLLM_CUDA(cudaEventCreateWithFlags(&P.copied, cudaEventDisableTiming));
@@ -523,15 +546,42 @@ static void run_job(sllm_load* L, PartJob& j) {
     SLLM_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
     cudaStream_t cs = j.ss->comm;
     SLLM_CUDA(cudaStreamWaitEvent(cs, j.ev[2], 0));
+    // Verification of what the round moved (K4 on the comm stream, after the collective).
+    // ZC: the rank's own chunks are verified inside K2; only received chunks are checked,
+    // per round.  CE: own and received chunks alike are verified in spans -- per root
+    // slice (BCAST) or over the partition (ALLGATHER rounds are contiguous) -- with the CE
+    // pipeline's span rule (<= kVerifyBytes per launch, shrinking towards the end), so a
+    // load is verified by a few long K4 launches instead of one per chunk and root.
+    const bool check = cfg.verify && idx.block;
+    const bool spans = check && cfg.mode == SLLM_MODE_CE;
+    sllm_load_config cfg_own = cfg;
+    if (spans) cfg_own.verify = 0;
+    struct Span { uint64_t lo = 0, hi = 0, end = 0; };
+    std::vector<Span> sp(ag ? 1 : R);
+    if (ag) {
+      sp[0].end = pr.length;
+    } else {
+      std::vector<uint64_t> sl(2 * R);
+      if (sllm_replica_slices(pr.length, C, R, sl.data()) != SLLM_OK) fail(SLLM_E_INVALID, "bad slices");
+      for (int q = 0; q < R; ++q) sp[q].end = sl[2 * q + 1];
+    }
+    auto extend = [&](Span& v, uint64_t a, uint64_t b) {
+      if (v.hi == v.lo) v.lo = a;
+      v.hi = b;
+      const uint64_t pending = v.hi - v.lo, remaining = v.end - v.hi;
+      if (remaining == 0 || pending >= kVerifyBytes || (pending >= kVerifyTailBytes && pending >= remaining)) {
+        verify_range(idx, cfg, j, v.lo, v.hi, cs);
+        v.lo = v.hi = 0;
+      }
+    };
     for (uint64_t r = 0; r < rounds; ++r) {
       full = 0;
       if (schedule(r, nullptr) != SLLM_OK) fail(SLLM_E_INVALID, "fan-out schedule failed");
       std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
       for (int q = 0; q < R; ++q) ranges[q] = {lohi[2 * q], lohi[2 * q + 1]};
       if (ranges[me].second > ranges[me].first) {  // this rank's own chunk of the round: PCIe
-        const uint64_t lo = ranges[me].first, hi = ranges[me].second;
-        (void)hi;
-        cudaStream_t done = issue_window(idx, cfg, j, P, r, lo / C, lo / C + 1, true);
+        const uint64_t lo = ranges[me].first;
+        cudaStream_t done = issue_window(idx, cfg_own, j, P, r, lo / C, lo / C + 1, true);
         SLLM_CUDA(cudaEventRecord(evk, done));
         SLLM_CUDA(cudaStreamWaitEvent(cs, evk, 0));
       }
@@ -539,15 +589,20 @@ static void run_job(sllm_load* L, PartJob& j) {
         if (q != me && ranges[q].second > ranges[q].first) j.fanout += ranges[q].second - ranges[q].first;
       if (ag && full) {  // NVLink: one in-place all-gather of the round's R whole chunks
         nccl_allgather_inplace(L->comm, ranges[0].first, C, j.dst_base, cs);
-        if (cfg.verify && idx.block) {  // the round is contiguous: what arrived is around our chunk
-          if (me > 0) verify_range(idx, cfg, j, ranges[0].first, ranges[me].first, cs);
-          if (me + 1 < R) verify_range(idx, cfg, j, ranges[me].second, ranges[R - 1].second, cs);
-        }
       } else {
         nccl_bcast_group(L->comm, ranges, j.dst_base, cs);  // NVLink: every root's chunk to every rank
-        if (cfg.verify && idx.block)
+      }
+      if (spans) {
+        for (int q = 0; q < R; ++q)
+          if (ranges[q].second > ranges[q].first) extend(sp[ag ? 0 : q], ranges[q].first, ranges[q].second);
+      } else if (check) {
+        if (ag && full) {  // the round is contiguous: what arrived is around our chunk
+          if (me > 0) verify_range(idx, cfg, j, ranges[0].first, ranges[me].first, cs);
+          if (me + 1 < R) verify_range(idx, cfg, j, ranges[me].second, ranges[R - 1].second, cs);
+        } else {
           for (int q = 0; q < R; ++q)
             if (q != me && ranges[q].second > ranges[q].first) verify_range(idx, cfg, j, ranges[q].first, ranges[q].second, cs);
+        }
       }
     }
     tails.push_back(cs);
@@ -584,8 +639,13 @@ static void run_job(sllm_load* L, PartJob& j) {
     if (R > 1) j.launches += 3;  // ready signal, ready wait, done signal
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
-    for (uint64_t k0 = 0, w = 0; k0 < nch; k0 += P.window, ++w)
-      issue_window(idx, cfg, j, P, w, k0, std::min(k0 + P.window, nch), k0 + P.window >= nch);
+    if (!P.plan.empty()) {  // SCATTER_CE from pinned DRAM: the window plan (every window fits a slot)
+      for (uint64_t w = 0; w < P.plan.size(); ++w)
+        issue_window(idx, cfg, j, P, w, P.plan[w].first, P.plan[w].second, w + 1 == P.plan.size());
+    } else {
+      for (uint64_t k0 = 0, w = 0; k0 < nch; k0 += P.window, ++w)
+        issue_window(idx, cfg, j, P, w, k0, std::min(k0 + P.window, nch), k0 + P.window >= nch);
+    }
   }
   // join every stream into s0, then let the caller's stream wait for the load
   join_streams(tails, s0);

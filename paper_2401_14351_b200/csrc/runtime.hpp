@@ -26,7 +26,9 @@ constexpr uint64_t kVerifyBytes = 2048ull << 20;  // CE mode: max bytes per veri
 constexpr uint64_t kVerifyTailBytes = 512ull << 20;  // CE mode: min span once the load's end is near
 constexpr uint64_t kAutoZeroCopyBytes = 256ull << 20;  // SLLM_MODE_AUTO: zero-copy below this per job
 constexpr int kDefaultEngine = 1;  // MatParams.engine of sllm_load_config.engine == 0
-constexpr uint64_t kScatterWindowBytes = 256ull << 20;  // SCATTER_CE: bytes per staging slot / K3 launch
+constexpr uint64_t kScatterWindowBytes = 1024ull << 20;  // SCATTER_CE: bytes per staging slot / K3 launch
+constexpr uint64_t kScatterTailBytes = 256ull << 20;     // SCATTER_CE: smallest window near the end
+constexpr uint64_t kScatterFileWindowBytes = 256ull << 20;  // SCATTER_CE from files: storage-ring window
 
 // Library-owned, per-GPU resources reused across loads (no allocation in the hot path).
 // Every running partition job leases its own stream set, so concurrent jobs on one GPU
