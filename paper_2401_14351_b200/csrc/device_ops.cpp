@@ -82,13 +82,18 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   const size_t seg_bytes = align_up(segs.size() * sizeof(Seg), 256);
   const size_t acc_bytes = align_up(nb * sizeof(BlockAcc), 256);
   const size_t tab = align_up(nb * 8, 256);
+  std::vector<uint32_t> gran;
+  gran_table(segs, pr.length, kGranShift, gran);
+  const size_t gran_bytes = align_up(gran.size() * 4, 256);
   void* scratch = nullptr;
-  SLLM_CUDA(cudaMallocAsync(&scratch, seg_bytes + acc_bytes + tab + 256, st));
+  SLLM_CUDA(cudaMallocAsync(&scratch, seg_bytes + acc_bytes + tab + 256 + gran_bytes, st));
   uint8_t* b = static_cast<uint8_t*>(scratch);
   Seg* d_segs = reinterpret_cast<Seg*>(b);
   BlockAcc* d_acc = reinterpret_cast<BlockAcc*>(b + seg_bytes);
   uint64_t* d_expect = reinterpret_cast<uint64_t*>(b + seg_bytes + acc_bytes);
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(b + seg_bytes + acc_bytes + tab);
+  uint32_t* d_gran = reinterpret_cast<uint32_t*>(b + seg_bytes + acc_bytes + tab + 256);
+  SLLM_CUDA(cudaMemcpyAsync(d_gran, gran.data(), gran.size() * 4, cudaMemcpyHostToDevice, st));
   SLLM_CUDA(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice, st));
   SLLM_CUDA(cudaMemsetAsync(d_acc, 0, acc_bytes, st));
   SLLM_CUDA(cudaMemsetAsync(d_bad, 0xFF, 8, st));
@@ -101,6 +106,8 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   mp.segs = d_segs;
   mp.seg_begin = 0;
   mp.seg_end = (uint32_t)segs.size();
+  mp.gran_seg = d_gran;
+  mp.gran_shift = kGranShift;
   mp.tile = idx->block ? (uint32_t)std::min<uint64_t>(kTile, idx->block) : kTile;
   mp.block = idx->block ? idx->block : kTile;
   mp.part_len = pr.length;

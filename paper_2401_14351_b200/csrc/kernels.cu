@@ -15,6 +15,8 @@
 // folded mod 2^32-1 after every segment, reduced over the CTA with warp shuffles, and
 // added atomically into the block's accumulator; the CTA finishing a block's last tile
 // finalises it and compares against the index's table.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace sllm {
@@ -180,6 +182,7 @@ constexpr int kTmaThreads = 32 * (kConsumerWarps + 2);  // producer, 8 consumers
 constexpr int kStoreLag = 4;                             // bulk-store groups in flight per CTA
 constexpr uint32_t kStageBytes = 16u << 10;
 constexpr int kStages = 12;
+constexpr uint64_t kMaxUnitBytes = 1ull << 20;  // default: whole 1 MiB blocks when the launch is balanced
 constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + 2 * kStages * sizeof(uint64_t);
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -233,6 +236,22 @@ __device__ __forceinline__ uint4 lds16(const uint8_t* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(smem_addr(p)));
   return r;
 }
+// Segment holding partition byte a: binary search over the launch's segments, narrowed to
+// a's granule when the host built the granule table (one dependent load instead of ~log2(n)).
+__device__ __forceinline__ uint32_t find_seg(const MatParams& p, uint64_t a) {
+  uint32_t lo = p.seg_begin, hi = p.seg_end;
+  if (p.gran_seg) {
+    const uint64_t g = a >> p.gran_shift;
+    lo = max(lo, p.gran_seg[g]);
+    hi = min(hi, p.gran_seg[g + 1] + 1);
+  }
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (p.segs[mid].off <= a) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory"); }
 
 template <bool kStore, bool kCheck>
@@ -287,12 +306,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
       int head = 0, cnt = 0;  // stages whose stores may still read smem, oldest first
       for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x) {
         const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
-        uint32_t lo = p.seg_begin, hi = p.seg_end;
-        while (hi - lo > 1) {
-          uint32_t mid = (lo + hi) >> 1;
-          if (p.segs[mid].off <= a) lo = mid; else hi = mid;
-        }
-        uint32_t cur = lo;
+        uint32_t cur = find_seg(p, a);
         Seg sg = p.segs[cur];
         for (uint64_t off = a; off < e; off += kStageBytes) {
           const uint64_t end = off + min((uint64_t)kStageBytes, e - off);
@@ -332,14 +346,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
     const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
     // segment holding byte a (same search in every thread: uniform, L1-cached)
     uint32_t cur = p.seg_begin;
-    if (kStore) {
-      uint32_t lo = p.seg_begin, hi = p.seg_end;
-      while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (p.segs[mid].off <= a) lo = mid; else hi = mid;
-      }
-      cur = lo;
-    }
+    if (kStore) cur = find_seg(p, a);
     Seg sg = kStore ? p.segs[cur] : Seg{0, 0, nullptr, 0};
     const uint64_t bstart = (u * unit / blk) * blk;  // first byte of this unit's checksum block
     unsigned long long A = 0, Bs = 0, Cs = 0;
@@ -527,6 +534,13 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
     return (double)U / (double)(((U + G - 1) / G) * G);
   };
   while (can_halve(q.split) && blk / (2 * q.split) >= (64u << 10) && balance(q.split) < 0.95) q.split *= 2;
+  // Largest unit (measurement knob SLLM_UNIT_KIB): smaller units shorten the launch's tail
+  // (the last CTA to finish is at most one unit behind) at 4 atomics per unit.
+  static const uint64_t max_unit = [] {
+    const char* e = getenv("SLLM_UNIT_KIB");
+    return (e && atoll(e) > 0) ? (uint64_t)atoll(e) << 10 : kMaxUnitBytes;
+  }();
+  while (can_halve(q.split) && blk / q.split > max_unit) q.split *= 2;
   if (!kCheck) q.split = 1;
   const uint64_t unit = blk / q.split;
   const uint64_t units = (p.hi + unit - 1) / unit - p.lo / unit;

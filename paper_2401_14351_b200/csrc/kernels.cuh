@@ -34,6 +34,10 @@ struct MatParams {
   uint64_t lo, hi;           // multiples of 16; lo is a multiple of `tile`
   const Seg* segs;           // segments covering [lo, hi), sorted by off
   uint32_t seg_begin, seg_end;
+  // optional (scatter modes): gran_seg[g] = last segment with off <= g << gran_shift, for
+  // g = 0..ceil(L >> gran_shift); bounds each unit's segment search to one granule's segments
+  const uint32_t* gran_seg;
+  uint32_t gran_shift;
   uint32_t tile;             // bytes per work tile (divides block; multiple of 16)
   uint64_t block;            // checksum block size B (0 = no checksum)
   uint64_t part_len;         // L_p

@@ -99,6 +99,8 @@ struct PartJob {
   uint32_t* d_err = nullptr;
   std::vector<Seg> segs;
   std::vector<uint32_t> chunk_seg;  // first segment of each chunk of [0, L)
+  std::vector<uint32_t> gran_seg;   // scatter: last segment with off <= g MiB (MatParams.gran_seg)
+  uint32_t* d_gran_seg = nullptr;
   // device scratch (one cudaMallocAsync block)
   void* scratch = nullptr;
   uint8_t* staging = nullptr;  // SCATTER_CE ring: n_streams slots of chunk_bytes (per job)
@@ -179,6 +181,8 @@ static void build_segments(const sllm_index& idx, PartJob& j, bool scatter, cons
     j.chunk_seg[k] = (uint32_t)s;
   }
   j.chunk_seg[nch] = (uint32_t)j.segs.size();
+  j.gran_seg.clear();
+  if (scatter) gran_table(j.segs, pr.length, kGranShift, j.gran_seg);
 }
 
 // Work tile: 64 KiB, or the checksum block when smaller (tiles never straddle blocks).
@@ -255,6 +259,8 @@ static MatParams window_params(const sllm_index& idx, const sllm_load_config& cf
   mp.lo = lo;
   mp.hi = hi;
   mp.segs = j.d_segs;
+  mp.gran_seg = j.d_gran_seg;
+  mp.gran_shift = kGranShift;
   mp.seg_begin = j.chunk_seg[k0];
   const uint64_t nch = j.chunk_seg.size() - 1;
   mp.seg_end = k1 < nch ? std::min<uint32_t>(j.chunk_seg[k1] + 1, (uint32_t)j.segs.size()) : (uint32_t)j.segs.size();
@@ -461,11 +467,14 @@ static void run_job(sllm_load* L, PartJob& j) {
   if (cfg.mode == SLLM_MODE_SCATTER_CE && !files) {
     // windows of P.window chunks, halving over the last two windows' worth of chunks down
     // to kScatterTailBytes, so the K3 that runs after the final copy is short
+    // (a partition of fewer than four full windows gets windows of a quarter of it, >= the
+    // tail size, so its first K3 starts early as well)
     const uint64_t wmin = std::min<uint64_t>(P.window, std::max<uint64_t>(1, kScatterTailBytes / cfg.chunk_bytes));
+    const uint64_t wide = std::min(P.window, std::max(wmin, ceil_div(nch_all, 4)));
     uint64_t widest = 1;
     for (uint64_t k0 = 0; k0 < nch_all;) {
       const uint64_t rem = nch_all - k0;
-      const uint64_t n = std::min(rem, rem > 2 * P.window ? P.window : std::max(wmin, (rem + 1) / 2));
+      const uint64_t n = std::min(rem, rem > 2 * wide ? wide : std::max(wmin, (rem + 1) / 2));
       P.plan.emplace_back(k0, k0 + n);
       widest = std::max(widest, n);
       k0 += n;
@@ -491,7 +500,8 @@ static void run_job(sllm_load* L, PartJob& j) {
   const size_t seg_bytes = align_up(j.segs.size() * sizeof(Seg), 256);
   const size_t acc_bytes = align_up(std::max<uint64_t>(nb, 1) * sizeof(BlockAcc), 256);
   const size_t tab_bytes = align_up(std::max<uint64_t>(nb, 1) * 8, 256);
-  const size_t total = seg_bytes + acc_bytes + 2 * tab_bytes + 256;
+  const size_t gran_bytes = align_up(j.gran_seg.size() * 4, 256);
+  const size_t total = seg_bytes + acc_bytes + 2 * tab_bytes + 256 + gran_bytes;
   if (j.origin) SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[3], 0));  // recorded by sllm_load_start
   SLLM_CUDA(cudaMallocAsync(&j.scratch, total, s0));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
@@ -506,6 +516,10 @@ static void run_job(sllm_load* L, PartJob& j) {
   j.d_cs = reinterpret_cast<uint64_t*>(base + seg_bytes + acc_bytes + tab_bytes);
   j.d_bad = reinterpret_cast<unsigned long long*>(base + seg_bytes + acc_bytes + 2 * tab_bytes);
   j.d_err = reinterpret_cast<uint32_t*>(j.d_bad + 1);
+  if (!j.gran_seg.empty()) {
+    j.d_gran_seg = reinterpret_cast<uint32_t*>(base + seg_bytes + acc_bytes + 2 * tab_bytes + 256);
+    SLLM_CUDA(cudaMemcpyAsync(j.d_gran_seg, j.gran_seg.data(), j.gran_seg.size() * 4, cudaMemcpyHostToDevice, s0));
+  }
   SLLM_CUDA(cudaMemcpyAsync(j.d_segs, j.segs.data(), j.segs.size() * sizeof(Seg), cudaMemcpyHostToDevice, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_acc, 0, acc_bytes, s0));
   SLLM_CUDA(cudaMemsetAsync(j.d_cs, 0, tab_bytes, s0));

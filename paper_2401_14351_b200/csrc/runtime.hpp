@@ -28,6 +28,7 @@ constexpr uint64_t kAutoZeroCopyBytes = 256ull << 20;  // SLLM_MODE_AUTO: zero-c
 constexpr int kDefaultEngine = 1;  // MatParams.engine of sllm_load_config.engine == 0
 constexpr uint64_t kScatterWindowBytes = 1024ull << 20;  // SCATTER_CE: bytes per staging slot / K3 launch
 constexpr uint64_t kScatterTailBytes = 256ull << 20;     // SCATTER_CE: smallest window near the end
+constexpr uint32_t kGranShift = 20;  // scatter granule table: one entry per MiB of partition
 constexpr uint64_t kScatterFileWindowBytes = 256ull << 20;  // SCATTER_CE from files: storage-ring window
 
 // Library-owned, per-GPU resources reused across loads (no allocation in the hot path).
@@ -93,7 +94,19 @@ uint8_t* comm_peer_base(const sllm_comm* c, int q);
 uint32_t* comm_peer_signal(const sllm_comm* c, int q);
 uint64_t comm_timeout_ns(const sllm_comm* c);
 uint32_t comm_next_epoch(sllm_comm* c);
-void comm_local_barrier(sllm_comm* c);  // host rendezvous of the group's in-process ranks
+void comm_local_barrier(sllm_comm* c);
+
+// out[g] = index of the last segment with off <= g << shift, g = 0..ceil(len >> shift)
+// (segs sorted by off, segs[0].off == 0) -- MatParams.gran_seg.
+inline void gran_table(const std::vector<Seg>& segs, uint64_t len, uint32_t shift, std::vector<uint32_t>& out) {
+  const uint64_t n = ((len + (1ull << shift) - 1) >> shift) + 1;
+  out.assign(n, 0);
+  size_t s = 0;
+  for (uint64_t g = 0; g < n; ++g) {
+    while (s + 1 < segs.size() && segs[s + 1].off <= (g << shift)) ++s;
+    out[g] = (uint32_t)s;
+  }
+}  // host rendezvous of the group's in-process ranks
 cudaStream_t comm_stream(sllm_comm* c, int s);
 
 }  // namespace sllm
