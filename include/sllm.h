@@ -238,9 +238,18 @@ typedef enum {
   SLLM_MODE_ZEROCOPY = 1,   /* SM-issued 16 B reads of host-mapped memory -> base+off, fused checksum */
   SLLM_MODE_SCATTER_CE = 2, /* copy engine into a staging ring, then index-driven scatter kernel */
   SLLM_MODE_SCATTER_ZC = 3, /* SM-issued host reads scattered straight into per-tensor buffers */
-  SLLM_MODE_AUTO = 4        /* contiguous: ZEROCOPY when every partition (fan-out: slice) this
+  SLLM_MODE_AUTO = 4,       /* contiguous: ZEROCOPY when every partition (fan-out: slice) this
                                call moves is < 256 MiB and device-mapped, else CE; the report's
                                `mode` says which ran */
+  SLLM_MODE_GDS = 5         /* sllm_load_files_start only, contiguous, no fan-out: GPUDirect
+                               Storage -- `io_threads` cuFileRead readers move part_<d>.bin
+                               straight into base+off (no pinned DRAM tier), K4 verifies the
+                               landed prefix in spans.  libcufile.so.0 is loaded lazily; without
+                               the nvidia-fs driver cuFile serves the reads in its compatibility
+                               mode.  SLLM_E_IO if cuFile cannot be opened or a read fails.
+                               Opt-in: SLLM_E_INVALID unless the environment sets
+                               SLLM_ENABLE_GDS=1 (cuFileDriverOpen hangs, uncancellably, on
+                               hosts where cuFile cannot probe the PCI topology). */
 } sllm_mode;
 
 /* Replicated checkpoint (one partition, every GPU gets a full replica): rank r of n moves

@@ -324,7 +324,7 @@ class PinnedCache:
 class LoadConfig:
     chunk_bytes: int = 16 << 20   # P:1279 "16MB" (read as MiB, Q9)
     n_streams: int = 2
-    mode: str = "ce"              # ce | zerocopy | scatter_ce | scatter_zc | auto (ce or zerocopy by size)
+    mode: str = "ce"              # ce | zerocopy | scatter_ce | scatter_zc | auto (ce or zerocopy by size) | gds (files)
     fanout: str = "none"          # none | bcast / allgather (NCCL) | p2p (fused NVLink stores)
     verify: bool = True
     ctas: int = 0
@@ -333,7 +333,7 @@ class LoadConfig:
 
     def to_c(self) -> _abi.LoadConfig:
         modes = {"ce": _abi.MODE_CE, "zerocopy": _abi.MODE_ZEROCOPY, "scatter_ce": _abi.MODE_SCATTER_CE,
-                 "scatter_zc": _abi.MODE_SCATTER_ZC, "auto": _abi.MODE_AUTO}
+                 "scatter_zc": _abi.MODE_SCATTER_ZC, "auto": _abi.MODE_AUTO, "gds": _abi.MODE_GDS}
         fan = {"none": _abi.FANOUT_NONE, "bcast": _abi.FANOUT_BCAST, "p2p": _abi.FANOUT_P2P,
                "allgather": _abi.FANOUT_ALLGATHER}
         return _abi.LoadConfig(self.chunk_bytes, self.n_streams, modes[self.mode], fan[self.fanout],

@@ -485,7 +485,7 @@ static void run_job(sllm_load* L, PartJob& j) {
     P.slot_bytes = std::min(P.window, nch_all) * cfg.chunk_bytes;
     P.nslot = (int)std::min<uint64_t>((uint64_t)P.nslot, ceil_div(nch_all, P.window));
   }
-  if (!j.file.empty())  // (a replicated load reads only its slice [lo, hi) from storage)
+  if (!j.file.empty() && cfg.mode != SLLM_MODE_GDS)  // (a replicated load reads only its slice [lo, hi) from storage)
     j.fsrc = file_source_open(j.file, j.lo, j.hi, P.window * cfg.chunk_bytes, j.io_threads, j.gpu);
   SLLM_CUDA(cudaEventCreateWithFlags(&P.copied, cudaEventDisableTiming));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
@@ -656,6 +656,26 @@ static void run_job(sllm_load* L, PartJob& j) {
     if (!P.plan.empty()) {  // SCATTER_CE from pinned DRAM: the window plan (every window fits a slot)
       for (uint64_t w = 0; w < P.plan.size(); ++w)
         issue_window(idx, cfg, j, P, w, P.plan[w].first, P.plan[w].second, w + 1 == P.plan.size());
+    } else if (cfg.mode == SLLM_MODE_GDS) {
+      // storage -> HBM with cuFile (gds.cpp); the landed prefix is verified in K4 spans on
+      // the kernel stream with the CE pipeline's span rule
+      SLLM_CUDA(cudaStreamSynchronize(s0));  // scratch and tables are in place before K4 runs
+      const bool check = cfg.verify && idx.block;
+      uint64_t v_lo = 0, v_hi = 0;
+      gds_read(j.file, j.gpu, j.dst_base, 0, pr.length, P.window * C, j.io_threads > 0 ? j.io_threads : 4,
+               [&](uint64_t a, uint64_t b) {
+                 if (!check) return;
+                 if (v_hi == v_lo) v_lo = a;
+                 v_hi = b;
+                 const uint64_t pending = v_hi - v_lo, remaining = pr.length - v_hi;
+                 if (remaining == 0 || pending >= kVerifyBytes || (pending >= kVerifyTailBytes && pending >= remaining)) {
+                   verify_range(idx, cfg, j, v_lo, v_hi, P.kern);
+                   v_lo = v_hi = 0;
+                 }
+               },
+               &j.storage_wait_ns);
+      j.transferred = j.storage_bytes = pr.length;
+      j.chunks = nch;
     } else {
       for (uint64_t k0 = 0, w = 0; k0 < nch; k0 += P.window, ++w)
         issue_window(idx, cfg, j, P, w, k0, std::min(k0 + P.window, nch), k0 + P.window >= nch);
@@ -667,7 +687,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   if (j.origin) gate_open_device(s0, j.gate);  // releases the caller's stream on the device
   j.t_issue_ns = now_ns() - t0;
   SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
-  if (j.fsrc) {
+  if (j.fsrc) {  // (GDS: set by the read loop)
     j.storage_bytes = file_source_bytes(*j.fsrc);
     j.storage_wait_ns = file_source_wait_ns(*j.fsrc);
   }
@@ -737,7 +757,14 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (cfg.chunk_bytes == 0) cfg.chunk_bytes = 16ull << 20;
   if (cfg.n_streams == 0) cfg.n_streams = 2;
   if (cfg.n_streams < 1 || cfg.n_streams > kMaxStreams) fail(SLLM_E_INVALID, "n_streams must be in 1..8");
-  if (cfg.mode < SLLM_MODE_CE || cfg.mode > SLLM_MODE_AUTO) fail(SLLM_E_INVALID, "unknown mode");
+  if (cfg.mode < SLLM_MODE_CE || cfg.mode > SLLM_MODE_GDS) fail(SLLM_E_INVALID, "unknown mode");
+  if (cfg.mode == SLLM_MODE_GDS && !dir) fail(SLLM_E_INVALID, "SLLM_MODE_GDS reads partition files (sllm_load_files_start)");
+  if (cfg.mode == SLLM_MODE_GDS && cfg.fanout != SLLM_FANOUT_NONE) fail(SLLM_E_INVALID, "SLLM_MODE_GDS has no fan-out");
+  if (cfg.mode == SLLM_MODE_GDS && !(getenv("SLLM_ENABLE_GDS") && atoi(getenv("SLLM_ENABLE_GDS")) == 1))
+    // cuFileDriverOpen never returns on hosts without nvidia-fs where its compatibility mode
+    // cannot probe the PCI topology (the VMs of this build: profiles/r01/gds_probe.log), and a
+    // hung driver open cannot be cancelled -- so GPUDirect Storage is opt-in per host.
+    fail(SLLM_E_INVALID, "SLLM_MODE_GDS is opt-in: set SLLM_ENABLE_GDS=1 on hosts with a working cuFile (nvidia-fs)");
   // AUTO: the copy engine unless every job moves less than kAutoZeroCopyBytes over PCIe from
   // device-mapped memory -- then the zero-copy kernel, whose lower fixed cost wins for small
   // loads (measured crossover).  Resolved below once the jobs are known.

@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <functional>
 #include <mutex>
 #include <thread>
 
@@ -95,6 +96,11 @@ uint32_t* comm_peer_signal(const sllm_comm* c, int q);
 uint64_t comm_timeout_ns(const sllm_comm* c);
 uint32_t comm_next_epoch(sllm_comm* c);
 void comm_local_barrier(sllm_comm* c);
+
+// GPUDirect Storage reads (gds.cpp): file bytes [lo, hi) -> dst + lo on `gpu`, `threads`
+// cuFile readers; landed(a, b) on the calling thread as the contiguous landed prefix grows.
+void gds_read(const std::string& path, int gpu, uint8_t* dst, uint64_t lo, uint64_t hi, uint64_t window, int threads,
+              const std::function<void(uint64_t, uint64_t)>& landed, uint64_t* wait_ns);
 
 // out[g] = index of the last segment with off <= g << shift, g = 0..ceil(len >> shift)
 // (segs sorted by off, segs[0].off == 0) -- MatParams.gran_seg.

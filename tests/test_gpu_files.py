@@ -86,3 +86,68 @@ def test_missing_file_is_io_error(tmp_path):
     idx2, lay2, _, payloads2 = write_ckpt(tmp_path, inv, seed)
     res = sllm.load_files(idx2, str(tmp_path), {0: 0}, sllm.LoadConfig())
     check(res, inv, payloads2, lay2, [0])
+
+
+# ---- GPUDirect Storage variant (SLLM_MODE_GDS: cuFileRead straight into HBM) ----------
+# cuFileDriverOpen never returns on the VMs this build runs on (no nvidia-fs; the
+# compatibility mode hangs probing the PCI topology: profiles/r01/gds_probe.log), so the
+# mode is opt-in (SLLM_ENABLE_GDS=1) and the read tests run only where it is set.
+
+GDS = os.environ.get("SLLM_ENABLE_GDS") == "1"
+
+
+def test_gds_is_opt_in_and_file_only(tmp_path, monkeypatch):
+    inv, seed = models.model_inventory("toy")
+    idx, lay, parts, payloads = write_ckpt(tmp_path, inv, seed)
+    monkeypatch.delenv("SLLM_ENABLE_GDS", raising=False)
+    with pytest.raises(sllm.SllmError) as ex:   # fails fast, never touches cuFile
+        sllm.load_files(idx, str(tmp_path), {0: 0}, sllm.LoadConfig(mode="gds"))
+    assert ex.value.status == 1 and "SLLM_ENABLE_GDS" in ex.value.message
+    from paper_2401_14351_b200 import workloads
+    idx2, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    monkeypatch.setenv("SLLM_ENABLE_GDS", "1")
+    with pytest.raises(sllm.SllmError) as ex:   # GDS reads files: not a pinned-source mode
+        sllm.load(idx2, bufs, {0: 0}, sllm.LoadConfig(mode="gds"))
+    assert ex.value.status == 1
+
+
+@pytest.mark.skipif(not GDS, reason="SLLM_ENABLE_GDS=1 not set (needs a host where cuFile opens)")
+@pytest.mark.parametrize("io_threads", [1, 4])
+def test_gds_toy(tmp_path, io_threads):
+    inv, seed = models.model_inventory("toy")
+    idx, lay, parts, payloads = write_ckpt(tmp_path, inv, seed)
+    res = sllm.load_files(idx, str(tmp_path), {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode="gds"),
+                          io_threads=io_threads)
+    assert res.report["storage_bytes"] == 13_594_624 and res.report["transferred_bytes"] == 13_594_624
+    assert res.report["mode"] == 5
+    check(res, inv, payloads, lay, [0])
+
+
+@pytest.mark.skipif(not GDS, reason="SLLM_ENABLE_GDS=1 not set (needs a host where cuFile opens)")
+def test_gds_two_partitions_many_windows(tmp_path):
+    """~1.1 GB over two partitions, 64 MiB windows, A = 16 (file lengths not 4 KiB multiples)."""
+    inv = models.llama2(1024, 36, 4096, 256, vocab=8192, tp=2)
+    inv = [models.TensorSpec(t.name, t.device, t.dtype, t.shape) for t in inv] + \
+          [models.TensorSpec("odd@0", 0, "u8", (33,)), models.TensorSpec("odd@1", 1, "f16", ())]
+    idx, lay, parts, payloads = write_ckpt(tmp_path, inv, 78, A=16, B=1 << 20)
+    res = sllm.load_files(idx, str(tmp_path), {0: 0, 1: 0}, sllm.LoadConfig(chunk_bytes=4 << 20, mode="gds"),
+                          io_threads=3)
+    check(res, inv, payloads, lay, [0, 1])
+
+
+@pytest.mark.skipif(not GDS, reason="SLLM_ENABLE_GDS=1 not set (needs a host where cuFile opens)")
+def test_gds_corruption_and_errors(tmp_path):
+    inv, seed = models.model_inventory("toy")
+    idx, lay, parts, payloads = write_ckpt(tmp_path, inv, seed)
+    path = tmp_path / "part_0.bin"
+    data = bytearray(open(path, "rb").read())
+    pos = 7 * (1 << 20) + 999
+    data[pos] ^= 0x01
+    open(path, "wb").write(bytes(data))
+    with pytest.raises(sllm.SllmError) as ex:
+        sllm.load_files(idx, str(tmp_path), {0: 0}, sllm.LoadConfig(chunk_bytes=2 << 20, mode="gds"))
+    assert ex.value.status == 9 and "block 7" in ex.value.message
+    os.remove(path)
+    with pytest.raises(sllm.SllmError) as ex:
+        sllm.load_files(idx, str(tmp_path), {0: 0}, sllm.LoadConfig(mode="gds"))
+    assert ex.value.status == 6
