@@ -314,6 +314,15 @@ static void copy_window(PartJob& j, int prof, uint8_t* dst, const uint8_t* wsrc,
   timed_end(e, j.cev, xs);
 }
 
+// Largest verification span (kVerifyBytes; SLLM_VERIFY_SPAN_MIB: measurement knob).
+static uint64_t verify_span_bytes() {
+  static const uint64_t v = [] {
+    const char* e = getenv("SLLM_VERIFY_SPAN_MIB");
+    return (e && atoll(e) > 0) ? (uint64_t)atoll(e) << 20 : kVerifyBytes;
+  }();
+  return v;
+}
+
 // Issue the window of chunks [k0, k1) of job j: the copy engine moves every chunk (one
 // batched submission), then ONE verify / scatter launch covers the window; zero-copy
 // modes issue one kernel for the window.  Returns the stream whose completion means
@@ -357,7 +366,7 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
         if (P.v_k1 == P.v_k0) P.v_k0 = k0;
         P.v_k1 = k1;
         const uint64_t pending = std::min(P.v_k1 * C, L) - P.v_k0 * C;
-        if (last || pending >= kVerifyBytes || (pending >= kVerifyTailBytes && pending >= L - hi)) {
+        if (last || pending >= verify_span_bytes() || (pending >= kVerifyTailBytes && pending >= L - hi)) {
           MatParams vp = window_params(idx, cfg, j, P.v_k0, P.v_k1, P.v_k0 * C, std::min(P.v_k1 * C, L));
           vp.src = j.dst_base;
           vp.src_origin = 0;
@@ -583,7 +592,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       if (v.hi == v.lo) v.lo = a;
       v.hi = b;
       const uint64_t pending = v.hi - v.lo, remaining = v.end - v.hi;
-      if (remaining == 0 || pending >= kVerifyBytes || (pending >= kVerifyTailBytes && pending >= remaining)) {
+      if (remaining == 0 || pending >= verify_span_bytes() || (pending >= kVerifyTailBytes && pending >= remaining)) {
         verify_range(idx, cfg, j, v.lo, v.hi, cs);
         v.lo = v.hi = 0;
       }
@@ -668,7 +677,7 @@ static void run_job(sllm_load* L, PartJob& j) {
                  if (v_hi == v_lo) v_lo = a;
                  v_hi = b;
                  const uint64_t pending = v_hi - v_lo, remaining = pr.length - v_hi;
-                 if (remaining == 0 || pending >= kVerifyBytes || (pending >= kVerifyTailBytes && pending >= remaining)) {
+                 if (remaining == 0 || pending >= verify_span_bytes() || (pending >= kVerifyTailBytes && pending >= remaining)) {
                    verify_range(idx, cfg, j, v_lo, v_hi, P.kern);
                    v_lo = v_hi = 0;
                  }
