@@ -90,7 +90,7 @@ class ClockSampler:
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,clocks.mem,clocks.max.mem")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
@@ -127,8 +127,11 @@ class ClockSampler:
             for k, n in enumerate(names):
                 if len(r) > 4 + k and r[4 + k].lower() == "active":
                     reasons.add(n)
+        num = lambda k: [float(r[k]) for r in self.rows if len(r) > k and r[k].replace(".", "").isdigit()]
+        mem, mem_max = num(8), num(9)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "mem_mhz": statistics.median(mem) if mem else None, "mem_max_mhz": max(mem_max) if mem_max else None}
 
 
 def peaks():
