@@ -123,6 +123,7 @@ struct PartJob {
   uint64_t storage_bytes = 0, storage_wait_ns = 0;  // file tier
   // profile: (start, end) event pairs around kernel launches / copies
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev, cev;
+  std::vector<uint64_t> kev_bytes;  // bytes covered by each timed kernel launch
   uint64_t kernel_bytes = 0;
   double kernel_ms = 0, copy_ms = 0;
   std::thread th;
@@ -214,7 +215,10 @@ static void launch(PartJob& j, bool prof, const MatParams& mp, MatKind kind, int
   auto e = timed_begin(prof, st);
   SLLM_CUDA(launch_materialise(mp, kind, ctas, st));
   timed_end(e, j.kev, st);
-  if (prof) j.kernel_bytes += mp.hi - mp.lo;
+  if (prof) {
+    j.kernel_bytes += mp.hi - mp.lo;
+    j.kev_bytes.push_back(mp.hi - mp.lo);
+  }
   j.launches++;
 }
 
@@ -329,6 +333,8 @@ static uint64_t verify_span_bytes() {
 // "the window is in place and verified" (the fan-out orders its broadcast after it).
 static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, Pipe& P, uint64_t w,
                                  uint64_t k0, uint64_t k1, bool last) {
+  NvtxRange nv("sllm/window p=%zu w=%llu chunks=[%llu,%llu)", j.p, (unsigned long long)w, (unsigned long long)k0,
+               (unsigned long long)k1);
   const bool check = cfg.verify && idx.block;
   const int prof = cfg.profile;
   const int ctas = cfg.ctas > 0 ? cfg.ctas : default_ctas(cfg.mode);
@@ -367,6 +373,8 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
         P.v_k1 = k1;
         const uint64_t pending = std::min(P.v_k1 * C, L) - P.v_k0 * C;
         if (last || pending >= verify_span_bytes() || (pending >= kVerifyTailBytes && pending >= L - hi)) {
+          NvtxRange nvv("sllm/verify/span [%llu,%llu)", (unsigned long long)(P.v_k0 * C),
+                        (unsigned long long)std::min(P.v_k1 * C, L));
           MatParams vp = window_params(idx, cfg, j, P.v_k0, P.v_k1, P.v_k0 * C, std::min(P.v_k1 * C, L));
           vp.src = j.dst_base;
           vp.src_origin = 0;
@@ -412,6 +420,7 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
 // Checksum-only verification of bytes that arrived through the fan-out.
 static void verify_range(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, uint64_t lo, uint64_t hi,
                          cudaStream_t st) {
+  NvtxRange nv("sllm/verify/range [%llu,%llu)", (unsigned long long)lo, (unsigned long long)hi);
   MatParams mp{};
   mp.src = j.dst_base;
   mp.lo = lo;
@@ -442,6 +451,7 @@ static void join_streams(const std::vector<cudaStream_t>& tails, cudaStream_t s0
 }
 
 static void run_job(sllm_load* L, PartJob& j) {
+  NvtxRange nv("sllm/partition p=%zu gpu=%d", j.p, j.gpu);
   const sllm_index& idx = *L->idx;
   const sllm_load_config& cfg = L->cfg;
   const PartRec& pr = idx.parts[j.p];
@@ -598,6 +608,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       }
     };
     for (uint64_t r = 0; r < rounds; ++r) {
+      NvtxRange nvr("sllm/fanout/round %llu", (unsigned long long)r);
       full = 0;
       if (schedule(r, nullptr) != SLLM_OK) fail(SLLM_E_INVALID, "fan-out schedule failed");
       std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
@@ -666,6 +677,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       for (uint64_t w = 0; w < P.plan.size(); ++w)
         issue_window(idx, cfg, j, P, w, P.plan[w].first, P.plan[w].second, w + 1 == P.plan.size());
     } else if (cfg.mode == SLLM_MODE_GDS) {
+      NvtxRange nvg("sllm/gds p=%zu", j.p);
       // storage -> HBM with cuFile (gds.cpp); the landed prefix is verified in K4 spans on
       // the kernel stream with the CE pipeline's span rule
       SLLM_CUDA(cudaStreamSynchronize(s0));  // scratch and tables are in place before K4 runs
@@ -706,17 +718,26 @@ static void run_job(sllm_load* L, PartJob& j) {
   j.h_bad = tail[0];
   j.h_err = (uint32_t)tail[1];
   SLLM_CUDA(cudaEventElapsedTime(&j.t_dev_ms, j.ev[0], j.ev[1]));
+  static const bool dump = getenv("SLLM_PROFILE_DUMP") != nullptr;  // per-launch timeline on stderr
   for (auto* v : {&j.kev, &j.cev}) {
     double sum = 0;
-    for (auto& e : *v) {
+    for (size_t i = 0; i < v->size(); ++i) {
+      auto& e = (*v)[i];
       float ms = 0;
       SLLM_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
       sum += ms;
+      if (dump && v == &j.kev) {
+        float at = 0;
+        SLLM_CUDA(cudaEventElapsedTime(&at, j.ev[0], e.first));
+        fprintf(stderr, "sllm-prof p=%zu kernel=%zu start_ms=%.4f ms=%.4f bytes=%llu GBps=%.1f\n", j.p, i, at, ms,
+                (unsigned long long)j.kev_bytes[i], j.kev_bytes[i] / (ms * 1e6));
+      }
       cudaEventDestroy(e.first);
       cudaEventDestroy(e.second);
     }
     (v == &j.kev ? j.kernel_ms : j.copy_ms) = sum;
     v->clear();
+    j.kev_bytes.clear();
   }
   cudaEventDestroy(P.copied);
   for (auto& e : P.freed) cudaEventDestroy(e);
@@ -758,6 +779,7 @@ using namespace sllm;
 sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_config* cfg_in, const void* const* host_src,
                                      const int32_t* gpu, void* const* dst_base, void* const* dst_tensor,
                                      void* const* stream, sllm_comm* comm, const char* dir, int32_t io_threads) {
+  NvtxRange nv("sllm/load_start");
   if (!idx) fail(SLLM_E_INVALID, "null index");
   if (!idx->sealed) fail(SLLM_E_INVALID, "index is planned but not sealed");
   sllm_load_config cfg{};
@@ -968,6 +990,7 @@ static void join_load(sllm_load* L) {
 }
 
 sllm_status sllm_load_wait_internal(sllm_load* L, sllm_load_report* rep) {
+  NvtxRange nv("sllm/load_wait");
   join_load(L);
   if (rep) *rep = L->rep;
   if (L->result != SLLM_OK) {

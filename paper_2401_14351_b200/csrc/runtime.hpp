@@ -8,10 +8,30 @@
 #include <mutex>
 #include <thread>
 
+#include <nvtx3/nvToolsExt.h>
+
+#include <cstdio>
+
 #include "common.hpp"
 #include "kernels.cuh"
 
 namespace sllm {
+
+// Host-side NVTX range around a load phase (SURVEY §5 tracing): "sllm/<phase> ...".  Free
+// unless a tool (ncu --nvtx, nsys) injects NVTX; lets ncu select e.g. only the verification
+// launches with --nvtx-include "sllm/verify/".
+struct NvtxRange {
+  template <class... A>
+  explicit NvtxRange(const char* fmt, A... a) {
+    char b[96];
+    snprintf(b, sizeof b, fmt, a...);
+    nvtxRangePushA(b);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 [[noreturn]] void cuda_fail(cudaError_t e, const char* what);
 #define SLLM_CUDA(call)                                   \
