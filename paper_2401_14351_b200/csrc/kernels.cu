@@ -15,6 +15,7 @@
 // folded mod 2^32-1 after every segment, reduced over the CTA with warp shuffles, and
 // added atomically into the block's accumulator; the CTA finishing a block's last tile
 // finalises it and compares against the index's table.
+#include <atomic>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -500,22 +501,29 @@ cudaError_t launch_gate_spin(const uint32_t* flag, uint32_t value, cudaStream_t 
 }
 
 static int num_sms() {
-  static int sm_count[64] = {};  // per device, queried once
+  static std::atomic<int> sm_count[64];  // per device, queried once (zero-initialised)
   int dev = 0;
   cudaGetDevice(&dev);
-  int& sms = sm_count[dev & 63];
-  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  int sms = sm_count[dev & 63].load(std::memory_order_relaxed);
+  if (!sms) {
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+    sm_count[dev & 63].store(sms, std::memory_order_relaxed);
+  }
   return sms;
 }
 
 template <bool kStore, bool kCheck>
 static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream) {
-  static bool configured = false;  // per template instance
-  if (!configured) {
+  // The dynamic shared-memory opt-in is a property of the kernel in each device's context:
+  // set it once per (template instance, device); worker threads of different GPUs race here.
+  static std::atomic<bool> configured[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!configured[dev & 63].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(materialise_tma_kernel<kStore, kCheck>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured[dev & 63].store(true, std::memory_order_release);
   }
   // Split checksum blocks into up to 16 units of >= one stage (16 KiB) while the launch
   // has fewer than two units per SM, so a 64 MiB window still covers every SM.
