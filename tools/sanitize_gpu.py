@@ -55,13 +55,44 @@ def main():
         del rs
     for c in comms:
         c.free()
+    # NCCL fan-outs with a 1-rank communicator (grouped broadcasts / in-place all-gathers)
+    comm = sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, 0)
+    for fanout in ("bcast", "allgather"):
+        for mode in ("ce", "zerocopy"):
+            res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=2 << 20, mode=mode, fanout=fanout), comm=comm)
+            assert np.array_equal(res._keep[3][0].cpu().numpy(), parts[0]), (fanout, mode)
+            n += 1
+            del res
+    comm.free()
+    # a ~0.5 GB checkpoint with 1 MiB chunks: several SCATTER_CE staging windows (the window
+    # plan) and the granule-bounded segment search over hundreds of segments
+    mid = models.llama2(1024, 12, 4096, 1024, vocab=32000)
+    midx, mbufs = workloads.build_pinned(mid, 9, 4096, 1 << 20)
+    for mode in ("scatter_ce", "scatter_zc"):
+        res = sllm.load(midx, mbufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode))
+        assert np.array_equal(res.block_checksums(0), midx.block_checksums(0)), mode
+        for e in (0, len(mid) // 2, len(mid) - 1):
+            t = mid[e]
+            got = res.tensors[t.name].reshape(-1).view(torch.uint8).cpu().numpy()
+            assert np.array_equal(got, payload.payload_bytes(9, e, t.nbytes)), (mode, t.name)
+        n += 1
+        del res
+    for b in mbufs.values():
+        b.free()
+    # standalone K3 (device-resident image -> per-tensor buffers)
+    img = torch.from_numpy(parts[0].copy()).cuda()
+    _, per = sllm.allocate(idx, {0: 0}, scatter=True)
+    sllm.materialise_device(idx, 0, img.data_ptr(), per)
+    for e, t in enumerate(inv):
+        assert np.array_equal(per[t.name].reshape(-1).view(torch.uint8).cpu().numpy(), pl[e]), t.name
+    del img, per
     # standalone kernels
     src = torch.from_numpy(parts[0].copy()).cuda()
     out = torch.zeros(idx.partitions[0].n_blocks, dtype=torch.int64, device="cuda")
     sllm.block_checksums_device(src.data_ptr(), L, 1 << 20, out.data_ptr())
     torch.cuda.synchronize()
     assert [int(v) & (2**64 - 1) for v in out.cpu().tolist()] == lay.checksums[0]
-    print(f"sanitize_gpu ok: {n} loads + standalone K4")
+    print(f"sanitize_gpu ok: {n} loads + standalone K3 + standalone K4")
 
 
 if __name__ == "__main__":
