@@ -166,10 +166,14 @@ def run_reference(args, rank, world):
     from synth import models, payload
 
     inv, seed = models.model_inventory(args.config)
-    budget = int(args.cpu_sample_gib * (1 << 30))
+    # per-step sample: --cpu-sample-gib, shrunk so that warmup + steps stay within ~60 GB of
+    # oracle work (~2 minutes on one core) whatever K and W the driver passes
+    budget = int(min(args.cpu_sample_gib * (1 << 30), max(256 << 20, 60e9 / max(1, args.warmup + args.steps))))
     # oracle converter over the sample's tensors (prefix of partition 0 in source order)
     lay = olayout.plan([(t.name, t.device, t.dtype, t.shape, t.nbytes) for t in inv], 4096, 1 << 20)
     d0 = lay.devices()[0]
+    first = min((e for e in lay.entries if e.device == d0), key=lambda e: e.offset)
+    budget = max(budget, -(-(first.offset + first.size) // (1 << 20)) << 20)  # at least one whole tensor
     keep = [i for i, e in enumerate(lay.entries) if e.device == d0 and e.offset + e.size <= budget]
     sub = [inv[i] for i in keep]
     tensors = [(t.name, t.device, t.dtype, t.shape, payload.payload_bytes(seed, keep[k], t.nbytes))
@@ -202,6 +206,9 @@ def cpu_baseline(args, bufs, idx, inv, seed):
     pinned partition: parse index, copy tensors, recompute and compare checksums."""
     from oracle import loader as oloader
     budget = int(args.cpu_sample_gib * (1 << 30))
+    p0 = sorted(bufs)[0]
+    first = min((t for t in idx.tensors if t.partition == p0), key=lambda t: t.offset)
+    budget = max(budget, -(-(first.offset + first.nbytes) // (1 << 20)) << 20)  # at least one whole tensor
     blob = idx.serialize()
     src = {idx.partitions[p].device: bufs[p].numpy() for p in bufs}
     t0 = time.perf_counter()
