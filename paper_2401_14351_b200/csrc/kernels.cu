@@ -179,6 +179,13 @@ __global__ void __launch_bounds__(kThreads) materialise_kernel(const MatParams p
 // flight per SM covers HBM latency (K3/K4) and, with a few CTAs, PCIe latency (K2).
 // ---------------------------------------------------------------------------------
 constexpr int kConsumerWarps = 8;
+// Stage release: one arrival per consumer warp after __syncwarp (default), or one per
+// consumer thread (SLLM_THREAD_ARRIVE=1: each thread's own reads directly before its own
+// release; the A/B for compute-sanitizer racecheck's model of the indirect syncwarp path).
+#ifndef SLLM_THREAD_ARRIVE
+#define SLLM_THREAD_ARRIVE 1
+#endif
+constexpr int kConsumerArrivals = SLLM_THREAD_ARRIVE ? 32 * kConsumerWarps : kConsumerWarps;
 constexpr int kTmaThreads = 32 * (kConsumerWarps + 2);  // producer, 8 consumers, bulk storer
 constexpr int kStoreLag = 4;                             // bulk-store groups in flight per CTA
 constexpr uint32_t kStageBytes = 16u << 10;
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kConsumerWarps + (bulk_store ? 1 : 0));
+      mbar_init(&empty[i], kConsumerArrivals + (bulk_store ? 1 : 0));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -291,6 +298,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
         for (uint64_t off = a; off < e; off += kStageBytes) {
           const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
           mbar_wait(&empty[stage], phase ^ 1);
+          // the consumers' generic-proxy reads of this stage (ordered before their empty
+          // arrivals) happen before the async-proxy TMA write that refills it
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_expect_tx(&full[stage], n);
           bulk_g2s(smem + (size_t)stage * kStageBytes, p.src + (off - p.src_origin), n, &full[stage]);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -382,8 +392,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           Cs += (unsigned long long)val.y + 2ull * val.z + 3ull * val.w;
         }
       }
+#if SLLM_THREAD_ARRIVE
+      mbar_arrive(&empty[stage]);  // every consumer thread releases its own reads of the stage
+#else
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
+#endif
       if (++stage == kStages) { stage = 0; phase ^= 1; }
       if (kCheck) {
         A = fold(A);

@@ -6,8 +6,8 @@ cuda:0 -- eight worker threads, eight pipelines, one PCIe link.
 
 Checked: every block checksum the GPU computes equals the index table (all 16,448 blocks
 of every partition), the index tables equal the oracle's Fletcher-64 on sampled blocks of
-the pinned source, sampled tensors equal their payload regenerated on the host, and the
-report's byte counts equal the oracle layout's.  Skipped when the box lacks the host RAM
+the pinned source, every byte of every tensor equals its payload regenerated on the host,
+and the report's byte counts equal the oracle layout's.  Skipped when the box lacks the host RAM
 or HBM to hold the checkpoint."""
 import os
 import time
@@ -29,6 +29,26 @@ from synth import models, payload  # noqa: E402
 
 def host_ram():
     return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+
+
+def every_tensor_equals_payload(tensors, inv, seed):
+    """Every byte of every loaded tensor against its payload regenerated on the host (O10,
+    the multi-threaded C generator pinned to the NumPy definition in test_synth.py), one
+    tensor at a time through a pinned scratch buffer; the comparison is torch.equal on the
+    device.  Returns the bytes compared."""
+    big = max(t.nbytes for t in inv)
+    host = torch.empty(big, dtype=torch.uint8, pin_memory=True)
+    dev = torch.empty(big, dtype=torch.uint8, device="cuda")
+    total = 0
+    for e, t in enumerate(inv):
+        n = t.nbytes
+        payload.payload_into([host.data_ptr()], [n], seed, [e])
+        dev[:n].copy_(host[:n])
+        got = tensors[t.name].reshape(-1).view(torch.uint8)
+        assert got.numel() == n and torch.equal(got, dev[:n]), t.name
+        total += n
+    del host, dev
+    return total
 
 
 @pytest.mark.parametrize("config,need", [("llama2-13b-tp2", 27e9), ("llama2-70b-tp8", 138e9)])
@@ -63,12 +83,17 @@ def test_partitioned_checkpoint_full_size(config, need):
         for p in parts:  # every block verified on the GPU, equal to the index table
             assert np.array_equal(res.block_checksums(p), idx.block_checksums(p)), p
         for e in sorted(set(rng.integers(0, len(inv), size=16).tolist()) | {0, len(inv) - 1}):
-            t = inv[e]
+            t = inv[e]  # sampled heads and tails against the NumPy definition itself
             n = min(t.nbytes, 1 << 20)
             got = res.tensors[t.name].reshape(-1).view(torch.uint8)[:n].cpu().numpy()
             assert np.array_equal(got, payload.payload_bytes(seed, e, t.nbytes)[:n]), t.name
             tail = res.tensors[t.name].reshape(-1).view(torch.uint8)[-n:].cpu().numpy()
             assert np.array_equal(tail, payload.payload_bytes(seed, e, t.nbytes)[-n:]), t.name
+        t0 = time.perf_counter()
+        checked = every_tensor_equals_payload(res.tensors, inv, seed)  # every tensor, every byte
+        assert checked == lay.payload_bytes
+        print(f"{config}: all {len(inv)} tensors ({checked / 1e9:.2f} GB) byte-equal to their payload "
+              f"({time.perf_counter() - t0:.1f} s)")
         del res
     finally:
         for b in bufs.values():
@@ -138,6 +163,8 @@ def test_replicated_opt30b_full_size_p2p():
                 v = results[r].tensors[t.name].reshape(-1).view(torch.uint8)
                 assert np.array_equal(v[:n].cpu().numpy(), want[:n]), (r, t.name)
                 assert np.array_equal(v[-n:].cpu().numpy(), want[-n:]), (r, t.name)
+        # every tensor of replica 0, every byte (replica 1 equals replica 0, checked above)
+        assert every_tensor_equals_payload(results[0].tensors, inv, seed) == lay.payload_bytes
         del results
     finally:
         if comms:

@@ -311,6 +311,16 @@ def test_opt67b_full_size_sampled():
             want = payload.payload_bytes(seed, e, t.nbytes)
             assert np.array_equal(got[:n].cpu().numpy(), want[:n]), (mode, t.name)
             assert np.array_equal(got[-n:].cpu().numpy(), want[-n:]), (mode, t.name)
+        # every tensor, every byte, against its payload regenerated on the host (C generator
+        # pinned to the NumPy definition), compared on the device
+        big = max(t.nbytes for t in inv)
+        host = torch.empty(big, dtype=torch.uint8, pin_memory=True)
+        dev = torch.empty(big, dtype=torch.uint8, device="cuda")
+        for e, t in enumerate(inv):
+            payload.payload_into([host.data_ptr()], [t.nbytes], seed, [e])
+            dev[:t.nbytes].copy_(host[:t.nbytes])
+            assert torch.equal(res.tensors[t.name].reshape(-1).view(torch.uint8), dev[:t.nbytes]), (mode, t.name)
+        del host, dev
         del res
         torch.cuda.empty_cache()
 

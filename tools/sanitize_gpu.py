@@ -24,6 +24,15 @@ def main():
     lay, parts = olayout.convert([(t.name, t.device, t.dtype, t.shape, p) for t, p in zip(inv, pl)], 4096, 1 << 20)
     n = 0
     only = os.environ.get("SANITIZE_ONLY")  # e.g. "zerocopy:tma" -- one load, nothing else
+    if only == "ring":  # the ~0.5 GB scatter loads only: every CTA wraps its stage ring many times
+        mid = models.llama2(1024, 12, 4096, 1024, vocab=32000)
+        midx, mbufs = workloads.build_pinned(mid, 9, 4096, 1 << 20)
+        for mode in ("scatter_ce", "scatter_zc", "ce"):
+            res = sllm.load(midx, mbufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode))
+            assert np.array_equal(res.block_checksums(0), midx.block_checksums(0)), mode
+            del res
+        print("sanitize_gpu ok: ring-wrap loads (scatter_ce, scatter_zc, ce)")
+        return
     for engine in ("tma", "ldg", "tma_store"):
         for mode in ("ce", "zerocopy", "scatter_ce", "scatter_zc"):
             if only and only != f"{mode}:{engine}":
