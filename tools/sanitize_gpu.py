@@ -27,11 +27,27 @@ def main():
     if only == "ring":  # the ~0.5 GB scatter loads only: every CTA wraps its stage ring many times
         mid = models.llama2(1024, 12, 4096, 1024, vocab=32000)
         midx, mbufs = workloads.build_pinned(mid, 9, 4096, 1 << 20)
-        for mode in ("scatter_ce", "scatter_zc", "ce"):
-            res = sllm.load(midx, mbufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode))
-            assert np.array_equal(res.block_checksums(0), midx.block_checksums(0)), mode
-            del res
-        print("sanitize_gpu ok: ring-wrap loads (scatter_ce, scatter_zc, ce)")
+        for engine in ("tma", "tma_store"):
+            for mode in ("scatter_ce", "scatter_zc", "ce", "zerocopy"):
+                res = sllm.load(midx, mbufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode, engine=engine))
+                assert np.array_equal(res.block_checksums(0), midx.block_checksums(0)), (engine, mode)
+                del res
+        # P2P fan-out group of 2 on this GPU: every vector also stored into the peer replica
+        L = midx.partitions[0].length
+        bases = [torch.empty(L, dtype=torch.uint8, device="cuda") for _ in range(2)]
+        sigs = [torch.zeros(4, dtype=torch.int32, device="cuda") for _ in range(2)]
+        comms = [sllm.Comm.peers(2, r, 0, [b.data_ptr() for b in bases], [s.data_ptr() for s in sigs], 60000)
+                 for r in range(2)]
+        for mode in ("ce", "zerocopy"):
+            cfg = sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode, fanout="p2p")
+            rs = [sllm.load_start(midx, mbufs, {0: 0}, cfg, {0: bases[r]}, None, None, comms[r]) for r in range(2)]
+            for r in rs:
+                r.wait()
+            assert torch.equal(bases[0], bases[1])
+            del rs
+        for c in comms:
+            c.free()
+        print("sanitize_gpu ok: ring-wrap loads (2 engines x 4 modes, P2P ce/zerocopy)")
         return
     for engine in ("tma", "ldg", "tma_store"):
         for mode in ("ce", "zerocopy", "scatter_ce", "scatter_zc"):
