@@ -83,3 +83,42 @@ def convert_safetensors(paths: Sequence[str], out_dir: str, device_of: Optional[
         return len(src.records)
     finally:
         src.close()
+
+
+# torch / NumPy dtypes -> the index's dtype names (include/sllm.h sllm_dtype)
+_NP_DTYPES = {np.dtype(np.float16): "f16", np.dtype(np.float32): "f32", np.dtype(np.int8): "i8",
+              np.dtype(np.uint8): "u8", np.dtype(np.int64): "i64"}
+
+
+def convert_state_dict(state_dict, out_dir: str, device_of: Optional[Callable[[str], int]] = None,
+                       align: int = 4096, block: int = 1 << 20, model_id: str = "") -> int:
+    """Convert an in-memory state dict (name -> CPU torch tensor or NumPy array, in the
+    dict's order = the layout's source order, Q2) into ``out_dir``/part_<d>.bin +
+    index.bin -- SURVEY §8(b)'s ``sllm.convert(state_dict_like, ...)``.  ``device_of(name)``
+    is the parallelism plan (which GPU each tensor goes to; default 0).  Tensors are
+    passed to sllm_convert by host pointer (made contiguous first when they are not); bf16
+    is supported for torch tensors.  Returns the tensor count; errors as sllm_convert."""
+    keep, records = [], []
+    for name, t in state_dict.items():
+        if hasattr(t, "detach"):  # torch.Tensor
+            import torch
+            if t.device.type != "cpu":
+                raise _abi.SllmError(_abi.E_INVALID, f"tensor '{name}' is on {t.device}; convert from host memory")
+            t = t.detach().contiguous()
+            if t.dtype == torch.bfloat16:
+                dt = "bf16"
+                arr = t.view(torch.int16).numpy()
+            else:
+                arr = t.numpy()
+                dt = _NP_DTYPES.get(arr.dtype)
+        else:
+            arr = np.ascontiguousarray(np.asarray(t))
+            dt = _NP_DTYPES.get(arr.dtype)
+        if dt is None:
+            raise _abi.SllmError(_abi.E_CONVERSION, f"tensor '{name}' has unsupported dtype {arr.dtype}")
+        arr = np.ascontiguousarray(arr)
+        keep.append(arr)
+        records.append((name, device_of(name) if device_of else 0, dt, tuple(int(s) for s in arr.shape),
+                        arr.ctypes.data if arr.size else 0, arr.nbytes))
+    convert(records, out_dir, align, block, model_id)
+    return len(records)

@@ -111,3 +111,48 @@ def test_cli_convert_and_info(tmp_path):
     assert r.returncode == 0, r.stderr
     info = json.loads(r.stdout)
     assert info["n_tensors"] == 7 and len(info["partitions"]) == 1
+
+
+def test_state_dict_front_end(tmp_path):
+    """sllm.convert of an in-memory state dict (torch CPU tensors incl. bf16 and a
+    non-contiguous view, NumPy arrays) split over two partitions by a parallelism plan:
+    read back by the oracle's index reader, layout re-derived by the oracle, every byte of
+    every tensor equal to the source, padding zero, block checksums = oracle Fletcher-64."""
+    torch = pytest.importorskip("torch")
+    g = torch.Generator().manual_seed(3)
+    base = torch.randn(64, 48, generator=g)
+    sd = {
+        "embed.weight@0": torch.randn(300, 64, generator=g).to(torch.float16),
+        "q.weight@0": torch.randn(64, 64, generator=g).to(torch.bfloat16),
+        "o.weight@1": base.t(),                                  # non-contiguous view (48 x 64 f32)
+        "norm.bias@1": np.random.default_rng(1).standard_normal(33).astype(np.float16),
+        "ids@1": torch.arange(17, dtype=torch.int64),
+        "scale@0": torch.tensor(0.5, dtype=torch.float16),       # scalar
+    }
+    dev = lambda n: int(n.rsplit("@", 1)[1])  # noqa: E731
+    from paper_2401_14351_b200 import formats
+    assert formats.convert_state_dict(sd, str(tmp_path), dev, 4096, 1 << 16, "sd") == len(sd)
+    lay = oindex.read(open(tmp_path / "index.bin", "rb").read())
+    ref = olayout.plan([(e.name, e.device, e.dtype, e.shape, e.size) for e in lay.entries], 4096, 1 << 16)
+    assert [(e.name, e.device, e.offset) for e in ref.entries] == [(e.name, e.device, e.offset) for e in lay.entries]
+    assert [e.name for e in lay.entries] == list(sd)          # source order kept
+    for d in lay.devices():
+        part = np.fromfile(tmp_path / f"part_{d}.bin", dtype=np.uint8)
+        covered = np.zeros(part.size, bool)
+        for e in lay.entries:
+            if e.device != d:
+                continue
+            t = sd[e.name]
+            if hasattr(t, "detach"):
+                t = t.contiguous()
+                want = (t.view(torch.int16) if t.dtype == torch.bfloat16 else t).numpy()
+            else:
+                want = t
+            want = np.ascontiguousarray(want).reshape(-1).view(np.uint8)
+            assert np.array_equal(part[e.offset:e.offset + e.size], want), e.name
+            covered[e.offset:e.offset + e.size] = True
+        assert not part[~covered].any()
+        assert lay.checksums[d] == fletcher.block_checksums(part, 1 << 16)
+    with pytest.raises(_abi.SllmError) as ex:                  # unsupported dtype
+        formats.convert_state_dict({"x": np.zeros(3, np.float64)}, str(tmp_path / "bad"))
+    assert ex.value.status == _abi.E_CONVERSION
