@@ -15,4 +15,12 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:mate
     -o $O/prof_pipeline_ce python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-standalone > $O/ncu_pipeline_ce.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:materialise_tma -s 1 -c 1 -f \
     -o $O/prof_pipeline_scatter_ce python bench.py --mode scatter_ce --steps 1 --warmup 0 --no-cpu-baseline --no-standalone > $O/ncu_pipeline_scatter_ce.log 2>&1
+
+# 2 ranks on the one GPU (gloo plumbing of the multi-rank paths; numbers share one PCIe link)
+for f in none p2p; do
+  SLLM_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+      --master-port 29531 bench.py --gpus 2 --steps 3 --warmup 3 --fanout $f --no-standalone --cpu-sample-gib 1 \
+      > $O/bench_n2_samegpu_$f.json 2> $O/bench_n2_samegpu_$f.err
+done
+
 ls -la $O > $O/ls.txt
