@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--chunk-mib", type=int, default=64)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--engine", default="tma", choices=["tma", "tma_store", "ldg"],
+                    help="kernel engine: TMA ring + vector stores (default), + TMA bulk stores, LDG/STG tiles")
     ap.add_argument("--all-partitions", action="store_true",
                     help="load every partition of a multi-partition config onto this rank's GPU (e.g. the whole "
                          "LLaMA-2-70B TP8 checkpoint on one B200)")
@@ -338,7 +340,7 @@ def main():
     parts = sorted(bufs)
     gpus = {p: gpu for p in parts}
     cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, n_streams=args.streams, mode=args.mode,
-                          ctas=args.ctas, profile=True, fanout=args.fanout)
+                          ctas=args.ctas, profile=True, fanout=args.fanout, engine=args.engine)
     # a2: destination allocation (reported separately, Q19)
     torch.cuda.synchronize()
     ta = time.perf_counter()
@@ -486,6 +488,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic",
                 "config": {"workload": args.config, "mode": args.mode, "fanout": args.fanout, "chunk_mib": args.chunk_mib,
+                           "engine": args.engine,
                            "streams": args.streams, "ctas": args.ctas, "partitions_per_gpu": len(parts),
                            "payload_bytes_per_gpu": payload_bytes,
                            "raw_bytes_per_gpu": raw_bytes, "verify": "fletcher64 per 1 MiB block, every block",
