@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--all-partitions", action="store_true",
                     help="load every partition of a multi-partition config onto this rank's GPU (e.g. the whole "
                          "LLaMA-2-70B TP8 checkpoint on one B200)")
+    ap.add_argument("--spread", action="store_true",
+                    help="with --all-partitions: partition p on GPU p %% (visible GPUs), all from this one process -- "
+                         "the paper's model manager loading every GPU of a server (P:721-727)")
     ap.add_argument("--fanout", default="none", choices=["none", "bcast", "allgather", "p2p"],
                     help="replicated checkpoint: every rank ends with a full replica; rank r reads slice r over "
                          "PCIe and the rest arrives over NVLink (bcast: NCCL broadcasts, allgather: in-place NCCL "
@@ -221,33 +224,43 @@ def cpu_baseline(args, bufs, idx, inv, seed):
                       f"copy every tensor, recompute+compare 1 MiB Fletcher-64 blocks; {dt:.1f} s"}
 
 
-def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1):
+def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1, gpus=None):
     """B_h2d(N): the copy engine's best host->device rate from the same pinned buffer into
     the same destination over >= 4 GiB: max of one 4 GiB
     cudaMemcpyAsync and back-to-back 64 MiB cudaMemcpyAsync calls on one stream, best of
     `reps` each.  Under torchrun every rep starts on a barrier so all N links (and the host
     DRAM / PCIe switches they share) are loaded at once; the aggregate is N * bytes / the
-    slowest rank's time.  Returns (aggregate GB/s, {method: aggregate GB/s})."""
-    p = sorted(bufs)[0]
-    n = min(gib << 30, bufs[p].nbytes)
-    src = bufs[p].torch()[:n]
-    dst = bases[p][:n]
+    slowest rank's time.  With partitions on several GPUs of this process (--spread) one
+    partition per GPU copies at once, aggregate = their bytes / the slowest GPU's time.
+    Returns (aggregate GB/s, {method: aggregate GB/s})."""
+    firsts = {}
+    for p in sorted(bufs):
+        firsts.setdefault(gpus[p] if gpus else torch.cuda.current_device(), p)
+    sizes = {g: min(gib << 30, bufs[p].nbytes) for g, p in firsts.items()}
     out = {}
-    for name, piece in (("single_4GiB", n), ("chunked_64MiB", 64 << 20)):
+    for name, piece in (("single_4GiB", None), ("chunked_64MiB", 64 << 20)):
         best = 0.0
         for _ in range(reps):
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
+            for g in firsts:
+                torch.cuda.synchronize(g)
             if world > 1:
                 import torch.distributed as dist
                 dist.barrier()
-            s.record()
-            for o in range(0, n, piece):
-                dst[o:o + piece].copy_(src[o:o + piece], non_blocking=True)
-            e.record()
-            e.synchronize()
-            ms = max_over_ranks(s.elapsed_time(e), world)
-            best = max(best, world * n / (ms * 1e-3) / 1e9)
+            evs = []
+            for g, p in firsts.items():
+                n = sizes[g]
+                src, dst = bufs[p].torch()[:n], bases[p][:n]
+                with torch.cuda.device(g):
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record()
+                    for o in range(0, n, piece or n):
+                        dst[o:o + (piece or n)].copy_(src[o:o + (piece or n)], non_blocking=True)
+                    e.record()
+                evs.append((s, e))
+            for s, e in evs:
+                e.synchronize()
+            ms = max_over_ranks(max(s.elapsed_time(e) for s, e in evs), world)
+            best = max(best, world * sum(sizes.values()) / (ms * 1e-3) / 1e9)
         out[name] = best
     return max(out.values()), out
 
@@ -333,12 +346,20 @@ def main():
         sel = list(range(n_parts))
     else:
         sel = [0] if world == 1 or n_parts == 1 else [rank]
-    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=sel,
-                                       gpu_of={p: gpu for p in sel})
+    if args.spread and (not args.all_partitions or world > 1 or replicated):
+        raise SystemExit("--spread goes with --all-partitions in a single process (no fan-out)")
+    ndev = torch.cuda.device_count() if args.spread else 1
+    gpu_map = {p: (p % ndev if args.spread else gpu) for p in sel}
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=sel, gpu_of=gpu_map)
     t_setup = time.perf_counter() - t0
     blob = idx.serialize()
     parts = sorted(bufs)
-    gpus = {p: gpu for p in parts}
+    gpus = {p: gpu_map[p] for p in parts}
+    used = sorted(set(gpus.values()))
+
+    def sync_all():
+        for g in used:
+            torch.cuda.synchronize(g)
     cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, n_streams=args.streams, mode=args.mode,
                           ctas=args.ctas, profile=True, fanout=args.fanout, engine=args.engine)
     # a2: destination allocation (reported separately, Q19)
@@ -351,9 +372,10 @@ def main():
     raw_bytes = sum(idx.partitions[p].length for p in parts)
 
     b_h2d, b_h2d_methods = h2d_peak(bufs, bases if not cfg.scatter else {p: torch.empty(min(4 << 30, idx.partitions[p].length),
-                                                                          dtype=torch.uint8, device=dev) for p in parts},
-                     torch, world=world)
+                                                                          dtype=torch.uint8, device=f"cuda:{gpus[p]}") for p in parts},
+                     torch, world=world, gpus=gpus)
     stream = torch.cuda.current_stream(gpu)
+    streams = {p: torch.cuda.current_stream(gpus[p]) for p in parts}
     comm = None
     if args.fanout == "p2p":      # peer group bound to every rank's replica (CUDA IPC over the process group)
         if world > 1:
@@ -367,7 +389,7 @@ def main():
     def step(prof: bool):
         c = sllm.LoadConfig(**{**cfg.__dict__, "profile": prof})
         ix = sllm.Index.from_bytes(blob)                  # a1: open + validate the index
-        res = sllm.load_start(ix, bufs, gpus, c, bases, per_tensor, {p: stream for p in parts}, comm)
+        res = sllm.load_start(ix, bufs, gpus, c, bases, per_tensor, streams, comm)
         return res, ix
 
     for _ in range(args.warmup):
@@ -377,22 +399,24 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    torch.cuda.synchronize()
-    evs = []
+    sync_all()
     reports = []
     with ClockSampler(gpu) as clk:
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        start.record(stream)
+        # one start/end pair per GPU this process loads (its caller stream is gated on the
+        # load); the step time is the slowest GPU's
+        marks = {g: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for g in used}
+        for g in used:
+            marks[g][0].record(torch.cuda.current_stream(g))
         for _ in range(args.steps):
             res, ix = step(not args.no_profile)
             reports.append(res.wait())
             del res, ix
-        end.record(stream)
-        torch.cuda.synchronize()
+        for g in used:
+            marks[g][1].record(torch.cuda.current_stream(g))
+        sync_all()
     if world > 1:
         dist.barrier()
-    ms_total = max_over_ranks(start.elapsed_time(end), world)
+    ms_total = max_over_ranks(max(a.elapsed_time(b) for a, b in marks.values()), world)
     ms_step = ms_total / args.steps
     # every rank ends the step with its own loaded model (sharded: its partition; replicated:
     # a full replica, of which it moved 1/N over PCIe)
@@ -406,7 +430,7 @@ def main():
         torch.cuda.empty_cache()
     e2e_t = []
     for _ in range(2):
-        torch.cuda.synchronize()
+        sync_all()
         t0 = time.perf_counter()
         ix = sllm.Index.from_bytes(blob)
         if comm is None:
@@ -415,7 +439,7 @@ def main():
             res = sllm.load_start(ix, bufs, gpus, sllm.LoadConfig(**{**cfg.__dict__, "profile": False}), bases,
                                   per_tensor, {p: stream for p in parts}, comm)
             res.wait()
-        torch.cuda.synchronize()
+        sync_all()
         e2e_t.append(time.perf_counter() - t0)
         del res, ix
     t_e2e = max_over_ranks(min(e2e_t), world)  # the job's end-to-end time is its slowest rank's
@@ -493,6 +517,7 @@ def main():
                            "payload_bytes_per_gpu": payload_bytes,
                            "raw_bytes_per_gpu": raw_bytes, "verify": "fletcher64 per 1 MiB block, every block",
                            "l2": f"inputs {raw_bytes / 1e9:.1f} GB per GPU >> 126 MB L2, no flush needed", "parallelism": f"replicated x{world} ({args.fanout})" if replicated else f"sharded x{world}",
+                           **({"spread": f"{len(parts)} partitions over GPUs {used} from one process"} if args.spread else {}),
                            **({"same_gpu_plumbing_check": "all ranks on cuda:0 (gloo); not a scaling number"}
                               if SAME_GPU and world > 1 else {})},
                 "time_to_loaded_model_s": ms_step * 1e-3, "t_alloc_s": t_alloc, "t_setup_s": t_setup,
