@@ -224,3 +224,18 @@ def test_allgather_schedule_properties():
             if r + 1 < len(rounds):
                 assert full
         assert pos == L
+
+
+def test_allgather_round_errors():
+    import ctypes as C
+    import paper_2401_14351_b200 as sllm
+    from paper_2401_14351_b200 import _abi
+    arr = (C.c_uint64 * 6)()
+    n, full = C.c_uint64(), C.c_int32()
+    assert sllm.lib().sllm_allgather_round(10 << 16, 1 << 16, 3, 0, arr, C.byref(n), C.byref(full)) == _abi.OK
+    assert n.value == 4 and full.value == 1
+    assert sllm.lib().sllm_allgather_round(10 << 16, 1 << 16, 3, 3, arr, None, C.byref(full)) == _abi.OK
+    assert full.value == 0 and [arr[i] for i in range(6)] == [9 << 16, 10 << 16, 0, 0, 0, 0]
+    assert sllm.lib().sllm_allgather_round(10 << 16, 1 << 16, 3, 4, arr, None, None) == _abi.E_LOOKUP
+    assert sllm.lib().sllm_allgather_round(10 << 16, 0, 3, 0, arr, None, None) == _abi.E_INVALID
+    assert sllm.lib().sllm_allgather_round(10 << 16, 1 << 16, 0, 0, arr, None, None) == _abi.E_INVALID
