@@ -400,6 +400,13 @@ SLLM_API sllm_status sllm_load_block_checksums(const sllm_load* load, size_t p, 
 /* Free worker state and scratch; waits for completion first.  Never frees caller memory. */
 SLLM_API void sllm_load_free(sllm_load* load);
 
+/* Release idle device memory the library keeps cached on `gpu` -- the stream-ordered pool
+ * holding per-load scratch and SCATTER_CE staging rings (up to 3 x 1 GiB), which finished
+ * loads return to the pool for the next load to reuse -- down to keep_bytes.  Synchronizes
+ * the device first; memory of loads still in flight is untouched.  For an inference engine
+ * that needs the HBM back (the GPU is shared with inference after the load). */
+SLLM_API sllm_status sllm_device_trim(int32_t gpu, uint64_t keep_bytes);
+
 /* ------------------------------------------------------------------------------------
  * Cross-process tensor handles (the inference process
  * "acquires the base addresses for each GPU (i.e., CUDA IPC handles) from the model

@@ -593,6 +593,12 @@ def load(index: Index, sources: Dict[int, object], gpus: Dict[int, int], config:
     return res
 
 
+def trim_device_cache(gpu: int, keep_bytes: int = 0) -> None:
+    """sllm_device_trim: hand the library's idle cached device memory (scratch, SCATTER_CE
+    staging) on ``gpu`` back to the driver, down to ``keep_bytes``."""
+    check(lib().sllm_device_trim(gpu, keep_bytes))
+
+
 def block_checksums_device(src_ptr: int, length: int, block: int, out_ptr: int, ctas: int = 0, stream=None) -> None:
     check(lib().sllm_block_checksums_device(C.c_void_p(src_ptr), length, block, C.c_void_p(out_ptr), ctas,
                                             C.c_void_p(stream.cuda_stream if stream is not None else 0)))

@@ -28,6 +28,7 @@ sllm_status sllm_load_wait_internal(sllm_load*, sllm_load_report*);
 void sllm_load_tensor_internal(const sllm_load*, const char*, sllm_tensor_handle*);
 void sllm_load_block_checksums_internal(sllm_load*, size_t, const uint64_t**);
 void sllm_load_free_internal(sllm_load*);
+void sllm_device_trim_internal(int32_t gpu, uint64_t keep_bytes);
 void sllm_comm_unique_id_internal(void*);
 sllm_comm* sllm_comm_init_rank_internal(const void*, int32_t, int32_t, int32_t);
 void sllm_comm_init_all_internal(const int32_t*, int32_t, sllm_comm**);
@@ -402,6 +403,10 @@ sllm_status sllm_load_block_checksums(const sllm_load* load, size_t p, const uin
 
 void sllm_load_free(sllm_load* load) {
   if (load) guard([&] { sllm_load_free_internal(load); });
+}
+
+sllm_status sllm_device_trim(int32_t gpu, uint64_t keep_bytes) {
+  return guard([&] { sllm_device_trim_internal(gpu, keep_bytes); });
 }
 
 sllm_status sllm_block_checksums_device(const void* src_dev, uint64_t len, uint64_t block, uint64_t* out_dev,

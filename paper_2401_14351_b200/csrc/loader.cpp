@@ -708,6 +708,14 @@ static void run_job(sllm_load* L, PartJob& j) {
   if (j.origin) gate_open_device(s0, j.gate);  // releases the caller's stream on the device
   j.t_issue_ns = now_ns() - t0;
   SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
+  if (j.staging) {
+    // The SCATTER_CE staging ring is not part of the loaded model: back to the stream-ordered
+    // pool as soon as the load is done (reusable by the next load at no cost; re-growing a
+    // trimmed pool per load measured 4x slower, profiles/r01/staging_trim_ab.json).  The pool
+    // keeps it cached until sllm_device_trim releases idle memory to the inference engine.
+    SLLM_CUDA(cudaFreeAsync(j.staging, s0));
+    j.staging = nullptr;
+  }
   if (j.fsrc) {  // (GDS: set by the read loop)
     j.storage_bytes = file_source_bytes(*j.fsrc);
     j.storage_wait_ns = file_source_wait_ns(*j.fsrc);
@@ -1052,4 +1060,13 @@ void sllm_load_free_internal(sllm_load* L) {
     gate_release(j.gate);
   }
   delete L;
+}
+
+void sllm_device_trim_internal(int32_t gpu, uint64_t keep_bytes) {
+  if (gpu < 0) fail(SLLM_E_INVALID, "bad GPU ordinal");
+  SLLM_CUDA(cudaSetDevice(gpu));
+  cudaMemPool_t pool;
+  SLLM_CUDA(cudaDeviceGetDefaultMemPool(&pool, gpu));
+  SLLM_CUDA(cudaDeviceSynchronize());  // frees queued by finished loads have taken effect
+  SLLM_CUDA(cudaMemPoolTrimTo(pool, (size_t)keep_bytes));
 }

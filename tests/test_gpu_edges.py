@@ -89,3 +89,21 @@ def test_smallest_blocks(mode):
     inv, seed = models.model_inventory("toy")
     inv = inv[:6] + inv[-2:]
     load_and_check(inv, seed, 16, 16, 64 << 10, mode)
+
+
+def test_device_trim_releases_staging():
+    """A finished SCATTER_CE load returns its staging ring to the stream-ordered pool (cached
+    for the next load); sllm_device_trim hands that idle memory back to the driver."""
+    mid = models.llama2(1024, 12, 4096, 1024, vocab=32000)  # ~0.53 GB, 3 staging windows
+    idx, bufs = workloads.build_pinned(mid, 9, 4096, 1 << 20)
+    res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=64 << 20, mode="scatter_ce"))
+    assert np.array_equal(res.block_checksums(0), idx.block_checksums(0))
+    torch.cuda.synchronize()
+    before = torch.cuda.mem_get_info(0)[0]
+    sllm.trim_device_cache(0)
+    after = torch.cuda.mem_get_info(0)[0]
+    assert after - before >= 256 << 20, (before, after)
+    res2 = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=64 << 20, mode="scatter_ce"))  # regrows
+    assert np.array_equal(res2.block_checksums(0), idx.block_checksums(0))
+    with pytest.raises(sllm.SllmError):
+        sllm.trim_device_cache(-1)
