@@ -365,6 +365,16 @@ class Comm:
         return cls(out.value)
 
     @classmethod
+    def init_all(cls, gpus: Sequence[int]) -> List["Comm"]:
+        """sllm_comm_init_all: one process driving several GPUs (ncclCommInitAll); handle i
+        belongs to gpus[i] and is rank i of the group."""
+        n = len(gpus)
+        arr = (C.c_int32 * n)(*[int(g) for g in gpus])
+        out = (C.c_void_p * n)()
+        check(lib().sllm_comm_init_all(arr, n, out))
+        return [cls(out[i]) for i in range(n)]
+
+    @classmethod
     def from_process_group(cls, gpu: int, group=None) -> "Comm":
         """Build the communicator over a torch.distributed group (id exchanged through it)."""
         import torch.distributed as dist

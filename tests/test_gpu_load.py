@@ -266,6 +266,20 @@ def test_fanout_single_rank_nccl():
     comm.free()
 
 
+def test_fanout_comm_init_all_single_process():
+    """The single-process communicator (sllm_comm_init_all, one handle per GPU of the
+    process) drives the NCCL fan-outs exactly like a per-rank communicator."""
+    inv, seed = models.model_inventory("toy")
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    lay, oparts, payloads = oracle_of(inv, seed, 4096, 1 << 20)
+    (comm,) = sllm.Comm.init_all([0])
+    for fanout in ("bcast", "allgather"):
+        cfg = sllm.LoadConfig(chunk_bytes=1 << 20, mode="ce", fanout=fanout)
+        res = sllm.load(idx, bufs, {0: 0}, cfg, comm=comm)
+        check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
+    comm.free()
+
+
 def test_allgather_rejects_files_and_peer_groups(tmp_path):
     inv, seed = models.model_inventory("toy")
     payloads = [payload.payload_bytes(seed, e, t.nbytes) for e, t in enumerate(inv)]
