@@ -1,0 +1,73 @@
+"""Soak test: many back-to-back loads through the public API (allocation + load + verify +
+free each time, rotating modes), watching device free memory and host RSS for leaks.
+
+    python tools/soak.py [--config opt-6.7b] [--loads 100]
+
+Prints one JSON line: loads, failures, seconds, device free memory and RSS before / after
+(after the library's idle cache is trimmed), and the GB/s range."""
+import argparse
+import json
+import os
+import resource
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def rss_gb():
+    with open("/proc/self/statm") as f:
+        return int(f.read().split()[1]) * os.sysconf("SC_PAGE_SIZE") / 1e9
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="opt-6.7b")
+    ap.add_argument("--loads", type=int, default=100)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    import paper_2401_14351_b200 as sllm
+    from paper_2401_14351_b200 import workloads
+    from synth import models
+
+    inv, seed = models.model_inventory(args.config)
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=[0], gpu_of={0: 0})
+    table = idx.block_checksums(0)
+    modes = ["ce", "zerocopy", "scatter_ce", "scatter_zc", "auto"]
+    # warm once per mode (pools, module load), then measure the baseline
+    for m in modes:
+        sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=64 << 20, mode=m)).free()
+    torch.cuda.synchronize()
+    sllm.trim_device_cache(0)
+    torch.cuda.empty_cache()
+    free0, rss0 = torch.cuda.mem_get_info(0)[0], rss_gb()
+    rates, failures, by_mode = [], 0, {m: [] for m in modes}
+    t0 = time.perf_counter()
+    for i in range(args.loads):
+        m = modes[i % len(modes)]
+        ts = time.perf_counter()
+        res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=64 << 20, mode=m))
+        rates.append(idx.partitions[0].length / (time.perf_counter() - ts) / 1e9)
+        by_mode[m].append(rates[-1])
+        if not np.array_equal(res.block_checksums(0), table):
+            failures += 1
+        res.free()
+        del res
+    dt = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    sllm.trim_device_cache(0)
+    torch.cuda.empty_cache()
+    free1, rss1 = torch.cuda.mem_get_info(0)[0], rss_gb()
+    print(json.dumps({"config": args.config, "loads": args.loads, "failures": failures, "seconds": dt,
+                      "GBps_min": min(rates), "GBps_median": float(np.median(rates)), "GBps_max": max(rates),
+                      "device_free_GB_before": free0 / 1e9, "device_free_GB_after": free1 / 1e9,
+                      "device_leak_GB": (free0 - free1) / 1e9, "rss_GB_before": rss0, "rss_GB_after": rss1,
+                      "maxrss_GB": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6,
+                      "per_mode_GBps": {m: {"min": min(v), "median": float(np.median(v)), "slowest_load": int(np.argmin(v))}
+                                        for m, v in by_mode.items() if v}}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
