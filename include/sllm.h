@@ -404,7 +404,8 @@ SLLM_API void sllm_load_free(sllm_load* load);
  * holding per-load scratch and SCATTER_CE staging rings (up to 3 x 1 GiB), which finished
  * loads return to the pool for the next load to reuse -- down to keep_bytes.  Synchronizes
  * the device first; memory of loads still in flight is untouched.  For an inference engine
- * that needs the HBM back (the GPU is shared with inference after the load). */
+ * that needs the HBM back (the GPU is shared with inference after the load).
+ * Errors: SLLM_E_INVALID for a negative ordinal, SLLM_E_CUDA if the device or pool call fails. */
 SLLM_API sllm_status sllm_device_trim(int32_t gpu, uint64_t keep_bytes);
 
 /* ------------------------------------------------------------------------------------
