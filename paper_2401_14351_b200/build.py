@@ -71,7 +71,8 @@ def build(force: bool = False, verbose: bool = False, sanitize: bool = False) ->
     os.makedirs(bdir, exist_ok=True)
     nvcc = _nvcc()
     host = "-fPIC,-O3,-fvisibility=hidden" if not sanitize else "-fPIC,-O1,-g,-fvisibility=hidden," + SAN_FLAGS
-    common = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", host,
+    extra = os.environ.get("SLLM_NVCC_DEFINES", "").split()  # A/B builds only, e.g. "-DSLLM_STAGE_KIB=32"
+    common = ["-O3", "-std=c++17", "-lineinfo", *ARCH, *extra, "-Xcompiler", host,
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()]
 
     def compile_one(src):

@@ -188,8 +188,17 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumerArrivals = SLLM_THREAD_ARRIVE ? 32 * kConsumerWarps : kConsumerWarps;
 constexpr int kTmaThreads = 32 * (kConsumerWarps + 2);  // producer, 8 consumers, bulk storer
 constexpr int kStoreLag = 4;                             // bulk-store groups in flight per CTA
-constexpr uint32_t kStageBytes = 16u << 10;
-constexpr int kStages = 12;
+// Ring geometry A/B (profiles/r01/ring_geometry_ab.jsonl): 16 KiB stages with the consumer
+// loop unrolled 4x beat 16 KiB / 8x and 32 KiB / 4x or 8x on K4 and K3 alike.
+#ifndef SLLM_CONSUMER_UNROLL
+#define SLLM_CONSUMER_UNROLL 4
+#endif
+#ifndef SLLM_STAGE_KIB
+#define SLLM_STAGE_KIB 16
+#endif
+constexpr int kConsumerUnroll = SLLM_CONSUMER_UNROLL;
+constexpr uint32_t kStageBytes = SLLM_STAGE_KIB << 10;  // ring: kStages x kStageBytes = 192 KiB
+constexpr int kStages = (192 << 10) / kStageBytes;
 constexpr uint64_t kMaxUnitBytes = 1ull << 20;  // default: whole 1 MiB blocks when the launch is balanced
 constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + 2 * kStages * sizeof(uint64_t);
 
@@ -366,7 +375,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
       const uint32_t w0 = (uint32_t)((off - bstart) >> 2);  // block word index of the stage start
       mbar_wait(&full[stage], phase);
       const uint8_t* sb = smem + (size_t)stage * kStageBytes;
-#pragma unroll 4
+#pragma unroll kConsumerUnroll
       for (uint32_t v = (uint32_t)ct * 16; v < n; v += 32 * kConsumerWarps * 16) {
         const uint4 val = lds16(sb + v);
         const uint64_t x = off + v;
