@@ -161,6 +161,17 @@ def ncu_traffic(mode, bytes_per_launch, key="traffic_over_algorithmic"):
     return cap[key] * bytes_per_launch, os.path.relpath(hits[-1], ROOT)
 
 
+def arm_config(args, world, parts, payload_bytes, raw_bytes, replicated, extra=None):
+    """The JSON line's `config` -- identical for our arm and the reference arm."""
+    return {"workload": args.config, "mode": args.mode, "fanout": args.fanout, "chunk_mib": args.chunk_mib,
+            "engine": args.engine, "streams": args.streams, "ctas": args.ctas, "partitions_per_gpu": parts,
+            "payload_bytes_per_gpu": payload_bytes, "raw_bytes_per_gpu": raw_bytes,
+            "verify": "fletcher64 per 1 MiB block, every block",
+            "l2": f"inputs {raw_bytes / 1e9:.1f} GB per GPU >> 126 MB L2, no flush needed",
+            "parallelism": f"replicated x{world} ({args.fanout})" if replicated else f"sharded x{world}",
+            **(extra or {})}
+
+
 def run_reference(args, rank, world):
     """Reference arm = the CPU oracle as it stands (oracle/loader.py) on this box's host
     cores, each step a bounded sample of the same workload."""
@@ -194,12 +205,16 @@ def run_reference(args, rank, world):
             times.append(dt)
     T = sum(times)
     v = got * args.steps / T / 1e9
+    n_parts = len(lay.devices())
+    sel = list(range(n_parts)) if args.all_partitions else [0]
+    devs = [lay.devices()[p] for p in sel]
+    ref_config = arm_config(args, world, len(sel), sum(e.size for e in lay.entries if e.device in devs),
+                            sum(lay.partitions[d] for d in devs), args.fanout != "none")
     line = {"metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": T / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{args.config} (oracle sample: first {got} payload bytes of partition 0)",
-                       "cache": "host-only"},
+            "config": ref_config,
             "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"parse index + copy + verify {got} B of {args.config} partition 0"},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -511,15 +526,10 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {"workload": args.config, "mode": args.mode, "fanout": args.fanout, "chunk_mib": args.chunk_mib,
-                           "engine": args.engine,
-                           "streams": args.streams, "ctas": args.ctas, "partitions_per_gpu": len(parts),
-                           "payload_bytes_per_gpu": payload_bytes,
-                           "raw_bytes_per_gpu": raw_bytes, "verify": "fletcher64 per 1 MiB block, every block",
-                           "l2": f"inputs {raw_bytes / 1e9:.1f} GB per GPU >> 126 MB L2, no flush needed", "parallelism": f"replicated x{world} ({args.fanout})" if replicated else f"sharded x{world}",
-                           **({"spread": f"{len(parts)} partitions over GPUs {used} from one process"} if args.spread else {}),
-                           **({"same_gpu_plumbing_check": "all ranks on cuda:0 (gloo); not a scaling number"}
-                              if SAME_GPU and world > 1 else {})},
+                "config": arm_config(args, world, len(parts), payload_bytes, raw_bytes, replicated, {
+                    **({"spread": f"{len(parts)} partitions over GPUs {used} from one process"} if args.spread else {}),
+                    **({"same_gpu_plumbing_check": "all ranks on cuda:0 (gloo); not a scaling number"}
+                       if SAME_GPU and world > 1 else {})}),
                 "time_to_loaded_model_s": ms_step * 1e-3, "t_alloc_s": t_alloc, "t_setup_s": t_setup,
                 "b_h2d_measured_GBps": b_h2d, "frac_h2d": pcie_rate / b_h2d,
                 "gpu_launches": int(rep["kernel_launches"]) * args.steps,
