@@ -62,8 +62,13 @@ typedef enum {
   SLLM_E_PEER = 12        /* P2P fan-out: a peer did not signal completion within the timeout   */
 } sllm_status;
 
-/* dtype codes; widths F16/BF16 2, F32 4, I8/U8 1, I64 8. */
-typedef enum { SLLM_F16 = 0, SLLM_BF16 = 1, SLLM_F32 = 2, SLLM_I8 = 3, SLLM_U8 = 4, SLLM_I64 = 5 } sllm_dtype;
+/* dtype codes (Q12: loading is dtype-agnostic -- the dtype fixes the
+ * element width the converter checks against the payload size, and the view type).  Widths:
+ * F16/BF16/I16 2, F32/I32 4, F64/I64 8, I8/U8/BOOL/F8_E4M3/F8_E5M2 1. */
+typedef enum {
+  SLLM_F16 = 0, SLLM_BF16 = 1, SLLM_F32 = 2, SLLM_I8 = 3, SLLM_U8 = 4, SLLM_I64 = 5,
+  SLLM_I32 = 6, SLLM_F64 = 7, SLLM_I16 = 8, SLLM_BOOL = 9, SLLM_F8_E4M3 = 10, SLLM_F8_E5M2 = 11
+} sllm_dtype;
 
 typedef struct sllm_index sllm_index; /* parsed / planned index (opaque)                  */
 typedef struct sllm_load sllm_load;   /* one in-flight load (opaque)                       */

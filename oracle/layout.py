@@ -19,8 +19,12 @@ import numpy as np
 from .errors import ConversionError, InvalidError, OracleLookupError
 
 # Oracle's own copy of the dtype table; deliberately not imported.
-WIDTH = {"f16": 2, "bf16": 2, "f32": 4, "i8": 1, "u8": 1, "i64": 8}
-CODE = {"f16": 0, "bf16": 1, "f32": 2, "i8": 3, "u8": 4, "i64": 5}
+# (Q12: SPEC's F16/F32/I8/I64 plus BF16/U8, and the remaining safetensors dtypes I32, F64, I16,
+# BOOL, F8_E4M3, F8_E5M2 -- the dtype only fixes the element width)
+WIDTH = {"f16": 2, "bf16": 2, "f32": 4, "i8": 1, "u8": 1, "i64": 8,
+         "i32": 4, "f64": 8, "i16": 2, "bool": 1, "f8e4m3": 1, "f8e5m2": 1}
+CODE = {"f16": 0, "bf16": 1, "f32": 2, "i8": 3, "u8": 4, "i64": 5,
+        "i32": 6, "f64": 7, "i16": 8, "bool": 9, "f8e4m3": 10, "f8e5m2": 11}
 NAME_OF_CODE = {v: k for k, v in CODE.items()}
 MAX_NDIM = 8
 

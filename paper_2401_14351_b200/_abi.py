@@ -20,7 +20,8 @@ STATUS = {0: "OK", 1: "INVALID", 2: "CONVERSION", 3: "FORMAT", 4: "LOOKUP", 5: "
 
 MODE_CE, MODE_ZEROCOPY, MODE_SCATTER_CE, MODE_SCATTER_ZC, MODE_AUTO, MODE_GDS = range(6)
 FANOUT_NONE, FANOUT_BCAST, FANOUT_P2P, FANOUT_ALLGATHER = range(4)
-DTYPE_CODE = {"f16": 0, "bf16": 1, "f32": 2, "i8": 3, "u8": 4, "i64": 5}
+DTYPE_CODE = {"f16": 0, "bf16": 1, "f32": 2, "i8": 3, "u8": 4, "i64": 5,
+              "i32": 6, "f64": 7, "i16": 8, "bool": 9, "f8e4m3": 10, "f8e5m2": 11}
 DTYPE_NAME = {v: k for k, v in DTYPE_CODE.items()}
 
 

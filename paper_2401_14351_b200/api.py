@@ -27,11 +27,14 @@ def _torch_dtypes():
     if _TORCH_DTYPE is None:
         import torch
         _TORCH_DTYPE = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32, "i8": torch.int8,
-                        "u8": torch.uint8, "i64": torch.int64}
+                        "u8": torch.uint8, "i64": torch.int64, "i32": torch.int32, "f64": torch.float64,
+                        "i16": torch.int16, "bool": torch.bool, "f8e4m3": torch.float8_e4m3fn,
+                        "f8e5m2": torch.float8_e5m2}
     return _TORCH_DTYPE
 
 
-WIDTH = {"f16": 2, "bf16": 2, "f32": 4, "i8": 1, "u8": 1, "i64": 8}
+WIDTH = {"f16": 2, "bf16": 2, "f32": 4, "i8": 1, "u8": 1, "i64": 8,
+         "i32": 4, "f64": 8, "i16": 2, "bool": 1, "f8e4m3": 1, "f8e5m2": 1}
 
 
 @dataclass(frozen=True)

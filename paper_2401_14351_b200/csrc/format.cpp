@@ -26,10 +26,10 @@ static constexpr uint32_t kFlagChecksums = 1;
 
 int dtype_width(int32_t dt) {
   switch (dt) {
-    case SLLM_F16: case SLLM_BF16: return 2;
-    case SLLM_F32: return 4;
-    case SLLM_I8: case SLLM_U8: return 1;
-    case SLLM_I64: return 8;
+    case SLLM_F16: case SLLM_BF16: case SLLM_I16: return 2;
+    case SLLM_F32: case SLLM_I32: return 4;
+    case SLLM_I8: case SLLM_U8: case SLLM_BOOL: case SLLM_F8_E4M3: case SLLM_F8_E5M2: return 1;
+    case SLLM_I64: case SLLM_F64: return 8;
     default: return 0;
   }
 }

@@ -21,7 +21,8 @@ from . import _abi
 from .api import convert
 
 # safetensors dtype tags -> the index's dtype names (include/sllm.h sllm_dtype)
-ST_DTYPES = {"F16": "f16", "BF16": "bf16", "F32": "f32", "I8": "i8", "U8": "u8", "I64": "i64"}
+ST_DTYPES = {"F16": "f16", "BF16": "bf16", "F32": "f32", "I8": "i8", "U8": "u8", "I64": "i64",
+             "I32": "i32", "F64": "f64", "I16": "i16", "BOOL": "bool", "F8_E4M3": "f8e4m3", "F8_E5M2": "f8e5m2"}
 
 
 def read_header(path: str) -> Tuple[dict, int]:
@@ -87,7 +88,8 @@ def convert_safetensors(paths: Sequence[str], out_dir: str, device_of: Optional[
 
 # torch / NumPy dtypes -> the index's dtype names (include/sllm.h sllm_dtype)
 _NP_DTYPES = {np.dtype(np.float16): "f16", np.dtype(np.float32): "f32", np.dtype(np.int8): "i8",
-              np.dtype(np.uint8): "u8", np.dtype(np.int64): "i64"}
+              np.dtype(np.uint8): "u8", np.dtype(np.int64): "i64", np.dtype(np.int32): "i32",
+              np.dtype(np.float64): "f64", np.dtype(np.int16): "i16", np.dtype(np.bool_): "bool"}
 
 
 def convert_state_dict(state_dict, out_dir: str, device_of: Optional[Callable[[str], int]] = None,
@@ -105,9 +107,11 @@ def convert_state_dict(state_dict, out_dir: str, device_of: Optional[Callable[[s
             if t.device.type != "cpu":
                 raise _abi.SllmError(_abi.E_INVALID, f"tensor '{name}' is on {t.device}; convert from host memory")
             t = t.detach().contiguous()
-            if t.dtype == torch.bfloat16:
-                dt = "bf16"
-                arr = t.view(torch.int16).numpy()
+            raw = {torch.bfloat16: ("bf16", torch.int16), torch.float8_e4m3fn: ("f8e4m3", torch.uint8),
+                   torch.float8_e5m2: ("f8e5m2", torch.uint8)}
+            if t.dtype in raw:  # no NumPy twin: hand over the bytes under a same-width integer view
+                dt = raw[t.dtype][0]
+                arr = t.view(raw[t.dtype][1]).numpy()
             else:
                 arr = t.numpy()
                 dt = _NP_DTYPES.get(arr.dtype)

@@ -27,6 +27,10 @@ def _tensors(seed):
         "model.ids": rng.integers(-2**40, 2**40, size=(17,), dtype=np.int64),
         "model.qweight": rng.integers(-128, 127, size=(40, 24), dtype=np.int8),
         "model.mask": rng.integers(0, 255, size=(9, 3), dtype=np.uint8),
+        "model.pos": rng.integers(-2**31, 2**31 - 1, size=(11,), dtype=np.int32),     # I32
+        "model.freq": rng.standard_normal((5, 3)),                                     # F64
+        "model.idx16": rng.integers(-2**15, 2**15 - 1, size=(7,), dtype=np.int16),    # I16
+        "model.flags": rng.integers(0, 2, size=(13,)).astype(bool),                    # BOOL
     }
 
 
@@ -63,7 +67,7 @@ def test_single_file(tmp_path):
     st_numpy.save_file(_tensors(0), f)
     out = str(tmp_path / "ckpt")
     n = formats.convert_safetensors([f], out, align=4096, block=1 << 16, model_id="st-test")
-    assert n == 7
+    assert n == 11
     _check(out, [f], lambda name: 0, 4096, 1 << 16)
 
 
@@ -80,8 +84,8 @@ def test_sharded_files_to_two_partitions(tmp_path):
 
 
 def test_rejects_unsupported_dtype_and_duplicates(tmp_path):
-    f = str(tmp_path / "f64.safetensors")
-    st_numpy.save_file({"w": np.zeros((4,), np.float64)}, f)
+    f = str(tmp_path / "u16.safetensors")
+    st_numpy.save_file({"w": np.zeros((4,), np.uint16)}, f)
     with pytest.raises(_abi.SllmError) as ex:
         formats.convert_safetensors([f], str(tmp_path / "o1"))
     assert ex.value.status == _abi.E_CONVERSION
@@ -104,13 +108,13 @@ def test_cli_convert_and_info(tmp_path):
     r = subprocess.run([sys.executable, "-m", "paper_2401_14351_b200", "convert", "--out", out, "--block", "65536", f],
                        capture_output=True, text=True, env=env)
     assert r.returncode == 0, r.stderr
-    assert json.loads(r.stdout)["converted_tensors"] == 7
+    assert json.loads(r.stdout)["converted_tensors"] == 11
     _check(out, [f], lambda name: 0, 4096, 1 << 16)
     r = subprocess.run([sys.executable, "-m", "paper_2401_14351_b200", "info", out], capture_output=True, text=True,
                        env=env)
     assert r.returncode == 0, r.stderr
     info = json.loads(r.stdout)
-    assert info["n_tensors"] == 7 and len(info["partitions"]) == 1
+    assert info["n_tensors"] == 11 and len(info["partitions"]) == 1
 
 
 def test_state_dict_front_end(tmp_path):
@@ -154,5 +158,5 @@ def test_state_dict_front_end(tmp_path):
         assert not part[~covered].any()
         assert lay.checksums[d] == fletcher.block_checksums(part, 1 << 16)
     with pytest.raises(_abi.SllmError) as ex:                  # unsupported dtype
-        formats.convert_state_dict({"x": np.zeros(3, np.float64)}, str(tmp_path / "bad"))
+        formats.convert_state_dict({"x": np.zeros(3, np.complex64)}, str(tmp_path / "bad"))
     assert ex.value.status == _abi.E_CONVERSION
