@@ -352,8 +352,12 @@ SLLM_API void sllm_comm_free(sllm_comm* comm);
  *                    tensors of unloaded partitions.  NULL array for contiguous modes.
  *   stream[p]      : optional caller cudaStream_t (as void*) for partition p.  The load is
  *                    ordered after work already queued on it, and the stream is made to
- *                    wait for the load's completion, so work queued on it after
- *                    sllm_load_start sees the loaded bytes.  NULL array/entry = no ordering.
+ *                    wait for the load's completion (an event wait, enqueued once the load's
+ *                    own work is all enqueued -- before this call returns), so work queued on
+ *                    it after sllm_load_start sees the loaded bytes.  (sllm_load_files_start
+ *                    and P2P groups with several ranks in one process enqueue that wait in
+ *                    sllm_load_wait instead: their issue waits on storage / on the peers.)
+ *                    NULL array/entry = no ordering.
  *   comm           : NULL unless cfg->fanout is BCAST / ALLGATHER (NCCL communicator) or
  *                    P2P (peer group); with BCAST or P2P, host_src[0] needs to hold (pinned)
  *                    only the rank's own slice [lo_r, hi_r) of sllm_replica_slices: bytes

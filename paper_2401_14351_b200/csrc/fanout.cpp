@@ -105,6 +105,11 @@ struct sllm_comm {
 namespace sllm {
 
 int comm_nranks(const sllm_comm* c) { return c->nranks; }
+int comm_local_members(const sllm_comm* c) {
+  if (!c || !c->local) return 1;
+  std::lock_guard<std::mutex> g(c->local->mu);
+  return c->local->members;
+}
 int comm_rank(const sllm_comm* c) { return c->rank; }
 int comm_device(const sllm_comm* c) { return c->dev; }
 bool comm_is_peers(const sllm_comm* c) { return c->peers; }

@@ -13,6 +13,7 @@
 // proceeds on the other stream(s) -- the pipeline "avoids synchronization for all data
 // on each storage tier" without host round trips.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
 #include <set>
 
@@ -82,6 +83,10 @@ static std::set<const void*> g_busy;
 struct PartJob {
   size_t p = 0;
   int gpu = 0;
+  // caller-stream ordering: `eager` jobs make the caller's stream wait on ev[1] before
+  // sllm_load_start returns (once the job has enqueued all its work); the others (file
+  // tier, in-process P2P groups: their issue waits on storage / on the peers) at wait()
+  bool eager = false, issue_signalled = false, issue_ok = false;
   const uint8_t* src = nullptr;      // host pointer (pinned)
   const uint8_t* src_dev = nullptr;  // its device-visible alias (zero-copy modes)
   uint8_t* dst_base = nullptr;
@@ -144,6 +149,8 @@ struct sllm_load {
   bool joined = false;
   sllm_status result = SLLM_OK;
   sllm_load_report rep{};
+  std::mutex issue_mu;                 // jobs report "all my work is enqueued" (or failed)
+  std::condition_variable issue_cv;
 };
 
 namespace sllm {
@@ -705,7 +712,11 @@ static void run_job(sllm_load* L, PartJob& j) {
   // join every stream into s0, then let the caller's stream wait for the load
   join_streams(tails, s0);
   SLLM_CUDA(cudaEventRecord(j.ev[1], s0));
-  if (j.origin) gate_open_device(s0, j.gate);  // releases the caller's stream on the device
+  {  // every command of this job is enqueued: the caller's stream may now wait on ev[1]
+    std::lock_guard<std::mutex> g(L->issue_mu);
+    j.issue_ok = j.issue_signalled = true;
+  }
+  L->issue_cv.notify_all();
   j.t_issue_ns = now_ns() - t0;
   SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
   if (j.staging) {
@@ -777,7 +788,11 @@ static void run_job_guarded(sllm_load* L, PartJob& j) {
     dc.release(j.ss);
     j.ss = nullptr;
   }
-  gate_open_host(j.gate);  // never leave the caller's stream waiting (success or failure)
+  {  // a job that failed before enqueueing everything still unblocks sllm_load_start
+    std::lock_guard<std::mutex> g(L->issue_mu);
+    j.issue_signalled = true;
+  }
+  L->issue_cv.notify_all();
 }
 
 }  // namespace sllm
@@ -927,16 +942,13 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
       for (auto& e : j.ev) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
       if (j.origin) {
         SLLM_CUDA(cudaEventRecord(j.ev[3], j.origin));
-        j.gate = gate_acquire();
-        gate_wait(j.origin, j.gate);
+        j.eager = j.file.empty() && !(cfg.fanout == SLLM_FANOUT_P2P && comm_local_members(comm) > 1);
       }
     }
   } catch (...) {
     std::lock_guard<std::mutex> g(g_busy_mu);
     for (const void* k : L->busy_keys) g_busy.erase(k);
     for (auto& j : L->jobs) {
-      gate_open_host(j.gate);
-      gate_release(j.gate);
       for (auto& e : j.ev)
         if (e) cudaEventDestroy(e);
     }
@@ -945,6 +957,24 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (cfg.fanout == SLLM_FANOUT_P2P)  // one epoch per collective load, taken in call order
     for (auto& j : L->jobs) j.epoch = comm_next_epoch(comm);
   for (auto& j : L->jobs) j.th = std::thread(run_job_guarded, L.get(), std::ref(j));
+  // Caller-stream ordering without a device-side gate: a stream waiting for work that is not
+  // yet enqueued can block, through the few hardware queues the context's streams share,
+  // work this or another load enqueues later (a deadlock seen with concurrent gated loads).
+  // So the caller's stream waits on ev[1] only once the job has enqueued everything -- the
+  // host issue of a pinned-source job takes well under the transfer time.
+  {
+    std::unique_lock<std::mutex> lk(L->issue_mu);
+    L->issue_cv.wait(lk, [&] {
+      for (auto& j : L->jobs)
+        if (j.eager && !j.issue_signalled) return false;
+      return true;
+    });
+  }
+  for (auto& j : L->jobs)
+    if (j.eager && j.issue_ok) {
+      cudaSetDevice(j.gpu);
+      if (cudaStreamWaitEvent(j.origin, j.ev[1], 0) != cudaSuccess) cudaGetLastError();
+    }
   return L.release();
 }
 
@@ -953,6 +983,11 @@ static void join_load(sllm_load* L) {
   for (auto& j : L->jobs)
     if (j.th.joinable()) j.th.join();
   L->joined = true;
+  for (auto& j : L->jobs)  // file tier / in-process P2P: the caller's stream is ordered here
+    if (j.origin && !j.eager && j.issue_ok) {
+      cudaSetDevice(j.gpu);
+      if (cudaStreamWaitEvent(j.origin, j.ev[1], 0) != cudaSuccess) cudaGetLastError();
+    }
   {
     std::lock_guard<std::mutex> g(g_busy_mu);
     for (const void* k : L->busy_keys) g_busy.erase(k);

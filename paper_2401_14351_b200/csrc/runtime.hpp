@@ -108,6 +108,7 @@ void nccl_bcast_group(sllm_comm* comm, const std::vector<std::pair<uint64_t, uin
                       uint8_t* buf, cudaStream_t s);
 void nccl_allgather_inplace(sllm_comm* comm, uint64_t lo, uint64_t count, uint8_t* buf, cudaStream_t s);
 int comm_nranks(const sllm_comm* c);
+int comm_local_members(const sllm_comm* c);  // ranks of c's P2P group living in this process
 int comm_rank(const sllm_comm* c);
 int comm_device(const sllm_comm* c);
 bool comm_is_peers(const sllm_comm* c);
