@@ -509,19 +509,6 @@ cudaError_t launch_peer_wait(const uint32_t* own, int nranks, int me, uint32_t e
   return cudaGetLastError();
 }
 
-__global__ void gate_spin_kernel(const uint32_t* flag, uint32_t value) {
-  for (;;) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if ((int32_t)(v - value) >= 0) return;
-    __nanosleep(2000);
-  }
-}
-
-cudaError_t launch_gate_spin(const uint32_t* flag, uint32_t value, cudaStream_t stream) {
-  gate_spin_kernel<<<1, 1, 0, stream>>>(flag, value);
-  return cudaGetLastError();
-}
 
 static int num_sms() {
   static std::atomic<int> sm_count[64];  // per device, queried once (zero-initialised)

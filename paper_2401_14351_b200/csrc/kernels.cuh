@@ -80,8 +80,5 @@ cudaError_t launch_peer_signal(const PeerSignal& s, uint32_t epoch, cudaStream_t
 cudaError_t launch_peer_wait(const uint32_t* own, int nranks, int me, uint32_t epoch, uint64_t timeout_ns,
                              uint32_t* err, cudaStream_t stream);
 
-// One-thread kernel that spins (with backoff) until *flag >= value in wrap-around order;
-// fallback for stream gates where cuStreamWaitValue32 is unavailable.
-cudaError_t launch_gate_spin(const uint32_t* flag, uint32_t value, cudaStream_t stream);
 
 }  // namespace sllm

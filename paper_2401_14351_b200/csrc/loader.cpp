@@ -115,7 +115,6 @@ struct PartJob {
   uint64_t* d_cs = nullptr;
   unsigned long long* d_bad = nullptr;
   cudaEvent_t ev[4] = {};  // start, end, setup, origin
-  Gate gate;               // caller-stream gate (origin != nullptr)
   // results
   std::vector<uint64_t> h_cs;
   bool h_cs_valid = false;
@@ -1092,7 +1091,6 @@ void sllm_load_free_internal(sllm_load* L) {
     if (j.staging) cudaFreeAsync(j.staging, dc.misc);
     for (auto& e : j.ev)
       if (e) cudaEventDestroy(e);
-    gate_release(j.gate);
   }
   delete L;
 }

@@ -88,19 +88,6 @@ void file_source_consumed(FileSource& f, uint64_t w, cudaStream_t s);  // slot r
 uint64_t file_source_bytes(FileSource& f);
 uint64_t file_source_wait_ns(FileSource& f);  // worker time blocked waiting for storage
 
-// ---- stream gates (gate.cpp) -------------------------------------------------------
-struct Gate {
-  int slot = -1;
-  uint32_t value = 0;
-  uint32_t* host = nullptr;
-  uint64_t dev = 0;
-};
-Gate gate_acquire();
-void gate_release(const Gate& g);
-void gate_wait(cudaStream_t s, const Gate& g);        // enqueue "wait until flag >= value"
-void gate_open_device(cudaStream_t s, const Gate& g); // enqueue "flag = value"
-void gate_open_host(const Gate& g);                    // flag = value, now
-
 // ---- NCCL (loaded with dlopen; only the calls the fan-out needs) -------------------
 struct Nccl;
 const Nccl& nccl();  // throws SLLM_E_NCCL if libnccl.so.2 cannot be loaded
