@@ -330,9 +330,10 @@ SLLM_API sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_com
  *                   overwritten by the next one), so back-to-back loads need no host barrier.
  *   timeout_ms    : how long a rank waits for its peers' completion signals before the
  *                   load fails with SLLM_E_PEER (0 = 60000).
- * A P2P load completes only when every rank's load has run, so several ranks driven from
- * one process must not pass the same caller stream (its gate would order them one after
- * the other and the first would wait for the others until the timeout).
+ * A P2P load completes only when every rank's load has run.  Ranks of one group that share
+ * a process rendezvous on the host around their peer signals (so no rank's device-side wait
+ * can block a peer's work queued behind it), and their caller streams are ordered after
+ * the load in sllm_load_wait, not in sllm_load_start.
  * The handle owns its streams; sllm_comm_free releases them (never the replicas). */
 SLLM_API sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
                                           uint32_t* const* peer_signal, uint64_t timeout_ms, sllm_comm** out);
