@@ -66,3 +66,48 @@ def test_concurrent_loads_from_threads():
         th.join(timeout=600)
     assert not any(th.is_alive() for th in threads), "a loader thread hung"
     assert not errors, errors
+
+
+def _file_worker(t, tmpdir, reps, errors):
+    try:
+        torch.cuda.set_device(0)
+        stream = torch.cuda.Stream()
+        rng = np.random.default_rng(9500 + t)
+        inv = models.random_inventory(rng, int(rng.integers(50, 400)), int(rng.integers(1, 3)), 40 << 20)
+        seed = 300 + t
+        payloads = [payload.payload_bytes(seed, e, x.nbytes) for e, x in enumerate(inv)]
+        d = f"{tmpdir}/ckpt{t}"
+        sllm.convert([(x.name, x.device, x.dtype, x.shape, p.ctypes.data) for x, p in zip(inv, payloads)], d,
+                     4096, 1 << 20, f"t{t}")
+        idx = sllm.Index.open(f"{d}/index.bin")
+        n = len(idx.partitions)
+        for r in range(reps):
+            mode = ["ce", "zerocopy", "scatter_ce", "scatter_zc"][(t + r) % 4]
+            with torch.cuda.stream(stream):
+                res = sllm.load_files(idx, d, {p: 0 for p in range(n)},
+                                      sllm.LoadConfig(chunk_bytes=2 << 20, mode=mode), io_threads=2,
+                                      stream_of_caller=bool(r % 2))
+            stream.synchronize()
+            for e, x in enumerate(inv):
+                got = res.tensors[x.name]
+                b = got.contiguous().view(torch.uint8).reshape(-1) if got.dim() else got.reshape(1).view(torch.uint8)
+                if not np.array_equal(b.cpu().numpy(), payloads[e]):
+                    errors.append((t, r, mode, x.name))
+                    return
+            del res
+    except Exception as ex:  # noqa: BLE001
+        errors.append((t, repr(ex)))
+
+
+def test_concurrent_file_and_pinned_loads(tmp_path):
+    """File-tier loads (caller stream ordered at wait) and pinned loads (ordered at start)
+    in flight together from separate threads."""
+    errors = []
+    threads = [threading.Thread(target=_worker, args=(t, 6, errors)) for t in range(3)] + \
+              [threading.Thread(target=_file_worker, args=(t, str(tmp_path), 4, errors)) for t in range(3)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=600)
+    assert not any(th.is_alive() for th in threads), "a loader thread hung"
+    assert not errors, errors
