@@ -26,6 +26,9 @@
  *     the matching *_close / *_free call.
  *   - thread safety: an sllm_index is immutable after open/seal and may be shared by
  *     threads; one sllm_load object must not be used from two threads at once.
+ *   - current device: calls that work on GPUs (load, comm, ipc, device helpers) may select
+ *     devices internally but restore the calling thread's current CUDA device before
+ *     returning.
  */
 #ifndef SLLM_H_
 #define SLLM_H_
@@ -95,6 +98,8 @@ typedef struct {
 /* Plan the layout of n tensors (no bytes move).  align: power of two >= 16.  block:
  * checksum block size, power of two multiple of align, or 0 for "no checksums".  The
  * returned index has zeroed checksum tables until sllm_index_seal / sllm_convert_into.
+ * align and block are at most 256 MiB (the device kernels' unfolded Fletcher sums stay below
+ * 2^64; Q8); sllm_index_open rejects larger values with SLLM_E_FORMAT.
  * Errors: SLLM_E_INVALID (align/block), SLLM_E_CONVERSION (names, sizes, dtype, dims). */
 SLLM_API sllm_status sllm_plan(const sllm_src_tensor* tensors, size_t n, uint64_t align, uint64_t block,
                       const char* model_id, sllm_index** out);
@@ -345,6 +350,9 @@ SLLM_API void sllm_comm_free(sllm_comm* comm);
  *   host_src[p]    : host pointer to partition p's bytes (pinned via sllm_host_alloc /
  *                    sllm_host_register or cudaHostAlloc), or NULL = partition not
  *                    loaded by this call.  For FANOUT_BCAST only the rank's slice is read.
+ *                    ZEROCOPY / SCATTER_ZC read it with 16-byte vector loads and TMA bulk
+ *                    copies: its device alias must be 16-byte aligned (else SLLM_E_INVALID;
+ *                    AUTO keeps the copy engine for a misaligned source).
  *   gpu[p]         : CUDA device ordinal for partition p (ignored if host_src[p] NULL).
  *   dst_base[p]    : device pointer, >= L_p bytes (contiguous modes and FANOUT); the
  *                    tensors are views base+offset.  May be NULL in scatter modes.

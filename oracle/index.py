@@ -25,7 +25,7 @@ from typing import Dict, List
 
 from . import fletcher
 from .errors import FormatError
-from .layout import CODE, NAME_OF_CODE, WIDTH, MAX_NDIM, Entry, Layout, is_pow2
+from .layout import CODE, NAME_OF_CODE, WIDTH, MAX_NDIM, MAX_BLOCK, Entry, Layout, is_pow2
 
 MAGIC = b"SLLMIDX1"
 VERSION = 1
@@ -118,6 +118,8 @@ def read(blob: bytes) -> Layout:
             raise FormatError(f"bad block size {B}")
     elif B != 0:
         raise FormatError("block size set without checksum flag")
+    if A > MAX_BLOCK or B > MAX_BLOCK:
+        raise FormatError("alignment / block size above 256 MiB (DESIGN.md Q8)")
     try:
         model_id = r.take(mid_len).decode("utf-8")
     except UnicodeDecodeError as ex:

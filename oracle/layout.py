@@ -27,6 +27,8 @@ CODE = {"f16": 0, "bf16": 1, "f32": 2, "i8": 3, "u8": 4, "i64": 5,
         "i32": 6, "f64": 7, "i16": 8, "bool": 9, "f8e4m3": 10, "f8e5m2": 11}
 NAME_OF_CODE = {v: k for k, v in CODE.items()}
 MAX_NDIM = 8
+# DESIGN.md Q8 (build limit): alignment and checksum block are at most 256 MiB
+MAX_BLOCK = 1 << 28
 
 
 def is_pow2(x: int) -> bool:
@@ -70,6 +72,8 @@ def validate_params(align: int, block: int) -> None:
         raise InvalidError(f"alignment {align} must be a power of two >= 16")
     if block != 0 and not (is_pow2(block) and block % align == 0):
         raise InvalidError(f"block {block} must be a power of two multiple of the alignment")
+    if align > MAX_BLOCK or block > MAX_BLOCK:
+        raise InvalidError("alignment / block size above 256 MiB (DESIGN.md Q8)")
 
 
 def validate_source(tensors: Sequence) -> None:

@@ -65,6 +65,31 @@ static sllm_status guard(F&& f) {
   }
 }
 
+// Entry points that select devices (cudaSetDevice on the caller's thread) restore the
+// caller's current device on exit: the device is per-thread driver state shared with every
+// other CUDA runtime in the process (PyTorch's included), so a load onto GPU 1 must not
+// leave the caller's thread on GPU 1.
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      dev = -1;
+    }
+  }
+  ~DeviceGuard() {
+    int now = -1;
+    if (dev >= 0 && (cudaGetDevice(&now) != cudaSuccess || now != dev)) cudaSetDevice(dev);
+    cudaGetLastError();
+  }
+};
+
+template <class F>
+static sllm_status guard_dev(F&& f) {
+  DeviceGuard dg;
+  return guard(std::forward<F>(f));
+}
+
 extern "C" {
 
 const char* sllm_last_error(void) { return t_last_error.c_str(); }
@@ -313,26 +338,26 @@ sllm_status sllm_comm_unique_id(void* id128) {
 }
 
 sllm_status sllm_comm_init_rank(const void* id128, int32_t nranks, int32_t rank, int32_t gpu, sllm_comm** out) {
-  return guard([&] {
+  return guard_dev([&] {
     if (!out) fail(SLLM_E_INVALID, "null out");
     *out = sllm_comm_init_rank_internal(id128, nranks, rank, gpu);
   });
 }
 
 sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_comm** out) {
-  return guard([&] { sllm_comm_init_all_internal(gpus, n, out); });
+  return guard_dev([&] { sllm_comm_init_all_internal(gpus, n, out); });
 }
 
 sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
                                  uint32_t* const* peer_signal, uint64_t timeout_ms, sllm_comm** out) {
-  return guard([&] {
+  return guard_dev([&] {
     if (!out) fail(SLLM_E_INVALID, "null out");
     *out = sllm_comm_init_peers_internal(nranks, rank, gpu, peer_base, peer_signal, timeout_ms);
   });
 }
 
 void sllm_comm_free(sllm_comm* c) {
-  guard([&] { sllm_comm_free_internal(c); });
+  guard_dev([&] { sllm_comm_free_internal(c); });
 }
 
 sllm_status sllm_cache_create(uint64_t capacity, int32_t gpu, int32_t pin, sllm_cache** out) {
@@ -363,7 +388,7 @@ void sllm_cache_destroy(sllm_cache* c) {
 sllm_status sllm_load_start(const sllm_index* idx, const sllm_load_config* cfg, const void* const* host_src,
                             const int32_t* gpu, void* const* dst_base, void* const* dst_tensor, void* const* stream,
                             sllm_comm* comm, sllm_load** out) {
-  return guard([&] {
+  return guard_dev([&] {
     if (!out) fail(SLLM_E_INVALID, "null out");
     *out = sllm_load_create_internal(idx, cfg, host_src, gpu, dst_base, dst_tensor, stream, comm, nullptr, 0);
   });
@@ -372,7 +397,7 @@ sllm_status sllm_load_start(const sllm_index* idx, const sllm_load_config* cfg, 
 sllm_status sllm_load_files_start(const sllm_index* idx, const sllm_load_config* cfg, const char* dir, const int32_t* gpu,
                                   void* const* dst_base, void* const* dst_tensor, void* const* stream, int32_t io_threads,
                                   sllm_comm* comm, sllm_load** out) {
-  return guard([&] {
+  return guard_dev([&] {
     if (!out || !dir) fail(SLLM_E_INVALID, "null argument");
     *out = sllm_load_create_internal(idx, cfg, nullptr, gpu, dst_base, dst_tensor, stream, comm, dir, io_threads);
   });
@@ -380,7 +405,7 @@ sllm_status sllm_load_files_start(const sllm_index* idx, const sllm_load_config*
 
 sllm_status sllm_load_wait(sllm_load* load, sllm_load_report* rep) {
   sllm_status st = SLLM_OK;
-  sllm_status g = guard([&] {
+  sllm_status g = guard_dev([&] {
     if (!load) fail(SLLM_E_INVALID, "null load");
     st = sllm_load_wait_internal(load, rep);
   });
@@ -395,28 +420,28 @@ sllm_status sllm_load_tensor(const sllm_load* load, const char* name, sllm_tenso
 }
 
 sllm_status sllm_load_block_checksums(const sllm_load* load, size_t p, const uint64_t** table) {
-  return guard([&] {
+  return guard_dev([&] {
     if (!load || !table) fail(SLLM_E_INVALID, "null argument");
     sllm_load_block_checksums_internal(const_cast<sllm_load*>(load), p, table);
   });
 }
 
 void sllm_load_free(sllm_load* load) {
-  if (load) guard([&] { sllm_load_free_internal(load); });
+  if (load) guard_dev([&] { sllm_load_free_internal(load); });
 }
 
 sllm_status sllm_device_trim(int32_t gpu, uint64_t keep_bytes) {
-  return guard([&] { sllm_device_trim_internal(gpu, keep_bytes); });
+  return guard_dev([&] { sllm_device_trim_internal(gpu, keep_bytes); });
 }
 
 sllm_status sllm_block_checksums_device(const void* src_dev, uint64_t len, uint64_t block, uint64_t* out_dev,
                                         int32_t ctas, void* stream) {
-  return guard([&] { block_checksums_device(src_dev, len, block, out_dev, ctas, static_cast<cudaStream_t>(stream)); });
+  return guard_dev([&] { block_checksums_device(src_dev, len, block, out_dev, ctas, static_cast<cudaStream_t>(stream)); });
 }
 
 sllm_status sllm_materialise_device(const sllm_index* idx, size_t p, const void* src_dev, void* const* dst_tensor,
                                     int32_t ctas, void* stream, uint64_t* bad_block, float* kernel_ms) {
-  return guard([&] {
+  return guard_dev([&] {
     uint64_t bad = materialise_device(idx, p, src_dev, dst_tensor, ctas, static_cast<cudaStream_t>(stream), kernel_ms);
     if (bad_block) *bad_block = bad;
     if (bad != ~0ull) fail(SLLM_E_CHECKSUM, "checksum mismatch in partition " + std::to_string(p) + ", block " +
@@ -435,18 +460,18 @@ void ipc_close(void* p);
 extern "C" {
 
 sllm_status sllm_ipc_export(const void* dev_ptr, uint64_t nbytes, sllm_ipc_region* out) {
-  return guard([&] { ipc_export(dev_ptr, nbytes, out); });
+  return guard_dev([&] { ipc_export(dev_ptr, nbytes, out); });
 }
 
 sllm_status sllm_ipc_open(const sllm_ipc_region* region, void** dev_ptr) {
-  return guard([&] {
+  return guard_dev([&] {
     if (!dev_ptr) fail(SLLM_E_INVALID, "null out");
     *dev_ptr = ipc_open(region);
   });
 }
 
 sllm_status sllm_ipc_close(void* dev_ptr) {
-  return guard([&] { ipc_close(dev_ptr); });
+  return guard_dev([&] { ipc_close(dev_ptr); });
 }
 
 }  // extern "C"

@@ -23,6 +23,11 @@ struct Error : std::runtime_error {
 
 void set_last_error(const std::string& m);
 
+// Largest alignment / checksum block (Q8): keeps the kernels' unfolded 64-bit
+// Fletcher partial sums (word index < 2^26 times a 16-byte vector sum < 2^34, 16 per tile)
+// below 2^64.
+constexpr uint64_t kMaxBlock = 256ull << 20;
+
 inline bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }

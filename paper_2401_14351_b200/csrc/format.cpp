@@ -101,6 +101,9 @@ static void check_params(uint64_t align, uint64_t block) {
   if (!is_pow2(align) || align < 16) fail(SLLM_E_INVALID, "alignment must be a power of two >= 16");
   if (block != 0 && (!is_pow2(block) || block % align))
     fail(SLLM_E_INVALID, "block size must be 0 or a power of two multiple of the alignment");
+  // DESIGN.md Q8: the device kernels fold their 64-bit Fletcher partial sums once per
+  // stage / tile; blocks up to kMaxBlock keep every unfolded sum below 2^64
+  if (align > kMaxBlock || block > kMaxBlock) fail(SLLM_E_INVALID, "alignment / block size above 256 MiB");
 }
 
 static void finish_index(sllm_index* idx) {
@@ -364,6 +367,7 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
   if (!is_pow2(A) || A < 16) fail(SLLM_E_FORMAT, "bad alignment");
   bool has_cs = flags & kFlagChecksums;
   if (has_cs ? (!is_pow2(B) || B % A) : B != 0) fail(SLLM_E_FORMAT, "bad block size");
+  if (A > kMaxBlock || B > kMaxBlock) fail(SLLM_E_FORMAT, "alignment / block size above 256 MiB");
   std::unique_ptr<sllm_index> idx(new sllm_index);
   idx->align = A;
   idx->block = B;
@@ -389,6 +393,9 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
   }
   std::vector<uint64_t> count(n_parts, 0);
   uint64_t sum = 0;
+  // every tensor record takes >= 32 bytes: a count the blob cannot hold is rejected before
+  // anything is sized by it
+  if ((uint64_t)n_tensors * 32 > r.limit - r.pos) fail(SLLM_E_FORMAT, "tensor count exceeds the index length");
   idx->tensors.reserve(n_tensors);
   for (uint32_t i = 0; i < n_tensors; ++i) {
     TensorRec t{};
@@ -437,6 +444,11 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
       const TensorRec& b = idx->tensors[pr.by_offset[k]];
       if (b.offset < a.offset + a.nbytes) fail(SLLM_E_FORMAT, "overlapping tensors '" + a.name + "' and '" + b.name + "'");
     }
+  {  // the checksum tables must fit the bytes left before the trailer (n_blocks comes from L_d)
+    unsigned __int128 need = 0;
+    for (const auto& pr : idx->parts) need += (unsigned __int128)pr.n_blocks * 8;
+    if (need > r.limit - r.pos) fail(SLLM_E_FORMAT, "checksum tables exceed the index length");
+  }
   for (auto& pr : idx->parts) {
     pr.checksums.resize(pr.n_blocks);
     for (auto& c : pr.checksums) {

@@ -30,8 +30,12 @@ struct Mapping {
   void* base;
   int refs;
 };
-static std::map<std::string, Mapping> g_maps;  // handle bytes -> mapping (one per allocation)
-static std::map<void*, std::string> g_open;    // returned pointer -> handle bytes
+struct Opened {
+  std::string key;
+  int count;
+};
+static std::map<std::string, Mapping> g_maps;  // handle bytes + device -> mapping (one per allocation)
+static std::map<void*, Opened> g_open;         // returned pointer -> its mapping, times returned
 
 void ipc_export(const void* ptr, uint64_t nbytes, sllm_ipc_region* out) {
   if (!ptr || !out) fail(SLLM_E_INVALID, "null argument");
@@ -64,6 +68,7 @@ void* ipc_open(const sllm_ipc_region* r) {
   if (!r) fail(SLLM_E_INVALID, "null region");
   SLLM_CUDA(cudaSetDevice(r->gpu));
   std::string key(reinterpret_cast<const char*>(r->handle), 64);
+  key.append(reinterpret_cast<const char*>(&r->gpu), sizeof r->gpu);  // mapped per importing device
   std::lock_guard<std::mutex> g(g_ipc_mu);
   auto it = g_maps.find(key);
   if (it == g_maps.end()) {
@@ -75,7 +80,8 @@ void* ipc_open(const sllm_ipc_region* r) {
   }
   it->second.refs++;
   void* p = static_cast<uint8_t*>(it->second.base) + r->offset;
-  g_open[p] = key;
+  auto o = g_open.emplace(p, Opened{key, 0}).first;  // the same region opened twice: counted
+  o->second.count++;
   return p;
 }
 
@@ -85,8 +91,8 @@ void ipc_close(void* p) {
     std::lock_guard<std::mutex> g(g_ipc_mu);
     auto it = g_open.find(p);
     if (it == g_open.end()) fail(SLLM_E_INVALID, "pointer was not returned by sllm_ipc_open");
-    auto m = g_maps.find(it->second);
-    g_open.erase(it);
+    auto m = g_maps.find(it->second.key);
+    if (--it->second.count == 0) g_open.erase(it);
     if (--m->second.refs > 0) return;
     base = m->second.base;
     g_maps.erase(m);

@@ -910,6 +910,12 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
       j.src_dev = at.devicePointer ? static_cast<const uint8_t*>(at.devicePointer) - probe : nullptr;
       if ((cfg.mode == SLLM_MODE_ZEROCOPY || cfg.mode == SLLM_MODE_SCATTER_ZC) && !j.src_dev)
         fail(SLLM_E_INVALID, "zero-copy modes need host memory mapped into the device address space");
+      // the zero-copy kernels read the source with 16-byte vector loads / TMA bulk copies from
+      // window starts (multiples of the chunk size): a misaligned source would fault the
+      // context, so it is refused here (AUTO then keeps the copy engine)
+      if ((cfg.mode == SLLM_MODE_ZEROCOPY || cfg.mode == SLLM_MODE_SCATTER_ZC) &&
+          (reinterpret_cast<uintptr_t>(j.src_dev) & 15))
+        fail(SLLM_E_INVALID, "zero-copy modes need a 16-byte aligned host source");
     }
     build_segments(*idx, j, scatter, L->dst_tensor, cfg.chunk_bytes);
     L->jobs.push_back(std::move(j));
@@ -917,7 +923,9 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   // busy set
   if (auto_mode) {
     bool zc = !L->jobs.empty();
-    for (auto& j : L->jobs) zc = zc && (j.hi - j.lo) < kAutoZeroCopyBytes && (j.src_dev || !j.file.empty());
+    for (auto& j : L->jobs)
+      zc = zc && (j.hi - j.lo) < kAutoZeroCopyBytes &&
+           (!j.file.empty() || (j.src_dev && !(reinterpret_cast<uintptr_t>(j.src_dev) & 15)));
     if (zc) cfg.mode = L->cfg.mode = SLLM_MODE_ZEROCOPY;
   }
   {

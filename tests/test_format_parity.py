@@ -168,3 +168,67 @@ def test_convert_to_files_and_read_partition(tmp_path):
         _abi.check(sllm.lib().sllm_host_read_partition(str(tmp_path).encode(), idx.handle, p,
                                                        ctypes.c_void_p(dst.ctypes.data), 3))
         assert np.array_equal(dst, oparts[d])
+
+
+def _reseal(b: bytearray) -> bytes:
+    """Recompute the index trailer (self-checksum) after a crafted edit -- the edit must be
+    caught by the structural checks, not by the checksum."""
+    import struct
+    n = len(b)
+    b[n - 16:n - 8] = struct.pack("<Q", fletcher.f64_closed(bytes(b[:n - 16])))
+    return bytes(b)
+
+
+def test_native_rejects_crafted_counts_before_sizing_by_them():
+    """A crafted (re-sealed) index whose tensor count or partition length promises more
+    records / checksum tables than the blob holds is rejected with SLLM_E_FORMAT before
+    anything is allocated by those counts (no multi-GB resize on bad input)."""
+    import struct
+    import time
+    inv = models.toy()
+    payloads = [payload.payload_bytes(0, e, t.nbytes) for e, t in enumerate(inv)]
+    lay, _ = _oracle_convert(inv, payloads, 4096, 1 << 20, "toy")
+    blob = oindex.write(lay)
+    # header: magic 8 | version 4 | flags 4 | A 8 | B 8 | n_parts 4 | n_tensors 4 @36
+    b = bytearray(blob)
+    b[36:40] = struct.pack("<I", 0xFFFFFFFF)
+    t0 = time.perf_counter()
+    with pytest.raises(sllm.SllmError) as ex:
+        sllm.Index.from_bytes(_reseal(b))
+    assert ex.value.status == 3 and "tensor count" in str(ex.value)
+    # partition record at 56 (header 52 B + "toy" padded to 8): L_d @64, n_blocks @80;
+    # L_d = 2^50 with the consistent n_blocks = 2^30 would need an 8 GiB checksum table
+    b = bytearray(blob)
+    b[64:72] = struct.pack("<Q", 1 << 50)
+    b[80:88] = struct.pack("<Q", (1 << 50) >> 20)
+    with pytest.raises(sllm.SllmError) as ex:
+        sllm.Index.from_bytes(_reseal(b))
+    assert ex.value.status == 3 and "checksum tables" in str(ex.value)
+    assert time.perf_counter() - t0 < 5
+
+
+@pytest.mark.parametrize("block", [1 << 28, 1 << 29])
+def test_block_size_cap_both_sides(block):
+    """DESIGN.md Q8 build limit: alignment and checksum block at most 256 MiB, in the oracle
+    and in the library alike (plan -> INVALID, a crafted index -> FORMAT)."""
+    from oracle.errors import FormatError, InvalidError
+    t = [("a", 0, "u8", (64,))]
+    if block <= 1 << 28:
+        assert sllm.Index.plan(t, 4096, block).info()["block"] == block
+        olayout.plan([(*x, 64) for x in t], 4096, block)
+        return
+    with pytest.raises(sllm.SllmError) as ex:
+        sllm.Index.plan(t, 4096, block)
+    assert ex.value.status == 1
+    with pytest.raises(InvalidError):
+        olayout.plan([(*x, 64) for x in t], 4096, block)
+    # a sealed index at the cap, its B field raised past it and re-sealed
+    import struct
+    lay, _ = _oracle_convert([models.toy()[0]], [payload.payload_bytes(0, 0, models.toy()[0].nbytes)], 4096, 1 << 28)
+    b = bytearray(oindex.write(lay))
+    b[24:32] = struct.pack("<Q", block)
+    with pytest.raises(sllm.SllmError) as ex:
+        sllm.Index.from_bytes(_reseal(b))
+    assert ex.value.status == 3
+    with pytest.raises(FormatError):
+        oindex.read(_reseal(b))
