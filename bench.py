@@ -2,26 +2,37 @@
 time-to-loaded-model at 1/2/4/8 B200 vs PCIe peak").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config opt-6.7b] [--mode zerocopy|ce|scatter_ce|scatter_zc]
-                    [--chunk-mib 16] [--streams 2] [--ctas 0] [--no-cpu-baseline]
+                    [--config auto|opt-6.7b|llama2-70b-tp8|...] [--mode ce|zerocopy|scatter_ce|scatter_zc]
+                    [--fanout none|bcast|allgather|p2p] [--chunk-mib 64] [--streams 2] [--ctas 0]
 
 A "step" is one pass of the whole hot path over the synthetic
 checkpoint already sitting in pinned host DRAM: open the index from its bytes (a1), plan
 chunks (a3), move every partition byte host->HBM (a4), materialise the tensors (a5),
-verify every 1 MiB block's Fletcher-64 on the GPU (a6), complete (a8).  Destinations
-are preallocated (a2; T_alloc is reported separately, Q19).  N=1 runs
-BASELINE configs[1] (OPT-6.7B-shaped, 13.3 GB fp16, 1 partition).  Under torchrun every
-rank loads its own copy of that partition from its own pinned buffer over its own PCIe
-link (weak scaling, no collective: SURVEY §8(e)).
+verify every 1 MiB block's Fletcher-64 on the GPU (a6), fan out (a7, replicated configs),
+complete (a8).  Destinations are preallocated (a2; T_alloc is reported separately,
+DESIGN.md Q19; `e2e` includes it).
+
+Launch.  One process per GPU.  `--gpus N` with N > 1 outside torchrun re-launches this
+script under `torch.distributed.run` with N ranks (and fails loudly when fewer than N GPUs
+are visible); under torchrun WORLD_SIZE must equal N.
+
+Workload (`--config auto`, the default) -- BASELINE.json configs by GPU count:
+  N = 1: configs[1] OPT-6.7B (13.3 GB, 1 partition);  N = 2: configs[2] LLaMA-2-13B TP2;
+  N = 4: LLaMA-2-70B TP4 (SURVEY C4s);  N = 8: configs[3] LLaMA-2-70B TP8 (the north star);
+  with a fan-out: configs[4] OPT-30B replicated.
+Sharded configs: rank r loads partition r (mod #partitions) over its own PCIe link from a
+NUMA-local pinned source, no collective (weak scaling).  Replicated: every
+rank ends with a full replica, each byte crossing PCIe once (a7).
 
 value = payload bytes loaded by all ranks / max-over-ranks device time (GB/s, 10^9).
-The partition (13.3 GB) is ~100x the 126 MB L2, so no flush is needed between steps.
+Per-GPU inputs (>= 13 GB) are ~100x the 126 MB L2: no flush between steps.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,15 +43,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "checkpoint load GB/s & time-to-loaded-model at 1/2/4/8 B200 vs PCIe peak"
+# BASELINE.json configs by GPU count (sharded); replicated runs use configs[4]
+CONFIG_FOR_N = {1: "opt-6.7b", 2: "llama2-13b-tp2", 4: "llama2-70b-tp4", 8: "llama2-70b-tp8"}
+REPLICATED_CONFIG = "opt-30b"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="opt-6.7b")
+    ap.add_argument("--config", default="auto",
+                    help="workload; auto = BASELINE config for the GPU count (see module docstring)")
     ap.add_argument("--mode", default="ce", choices=["ce", "zerocopy", "scatter_ce", "scatter_zc"])
     ap.add_argument("--chunk-mib", type=int, default=64)
     ap.add_argument("--streams", type=int, default=2)
@@ -56,12 +71,18 @@ def parse():
     ap.add_argument("--fanout", default="none", choices=["none", "bcast", "allgather", "p2p"],
                     help="replicated checkpoint: every rank ends with a full replica; rank r reads slice r over "
                          "PCIe and the rest arrives over NVLink (bcast: NCCL broadcasts, allgather: in-place NCCL "
-                         "all-gather per round of round-robin chunks, p2p: fused peer stores)")
-    ap.add_argument("--cpu-sample-gib", type=float, default=4.0)
+                         "all-gathers, p2p: fused peer stores)")
+    ap.add_argument("--cpu-sample-gib", type=float, default=2.0,
+                    help="oracle sample per partition (cpu_baseline and --impl reference)")
+    ap.add_argument("--cpu-reps", type=int, default=3, help="timed oracle reps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-standalone", action="store_true")
+    ap.add_argument("--no-baselines", action="store_true", help="replicated runs: skip the naive / root-broadcast lines")
     ap.add_argument("--no-profile", action="store_true", help="no per-launch CUDA events in the timed region")
-    return ap.parse_args()
+    ap.add_argument("--plumbing", action="store_true",
+                    help="CPU-only dry run of the launch / rank / max-over-ranks plumbing (gloo, host memcpy in place "
+                         "of the load; not a measurement)")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -78,16 +99,62 @@ def gpu_of(local):
     return 0 if SAME_GPU else local
 
 
-def max_over_ranks(x: float, world: int) -> float:
-    """Max of a per-rank float over the job (device tensor on NCCL, host tensor on gloo)."""
+def resolve_config(args, world: int) -> str:
+    if args.config != "auto":
+        return args.config
+    if args.fanout != "none":
+        return REPLICATED_CONFIG
+    return CONFIG_FOR_N.get(world, CONFIG_FOR_N[1])
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def fail_loudly(msg: str, code: int = 2):
+    print(json.dumps({"metric": METRIC, "error": msg}), file=sys.stderr, flush=True)
+    raise SystemExit(code)
+
+
+def visible_gpus() -> int:
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def maybe_self_launch(args, argv) -> None:
+    """`--gpus N` (N > 1) outside torchrun: re-launch under torch.distributed.run with N ranks
+    (one process per GPU), rendezvous on 127.0.0.1; exit with the launcher's status."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    if not args.plumbing and not SAME_GPU and args.impl == "ours":
+        n = visible_gpus()
+        if n < args.gpus:
+            fail_loudly(f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {n}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *argv]
+    raise SystemExit(subprocess.run(cmd).returncode)
+
+
+def max_over_ranks(x, world: int):
+    """Max of a per-rank float (or list of floats) over the job."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
     nccl = dist.get_backend() == "nccl"
-    t = torch.tensor([x], dtype=torch.float64, device=torch.cuda.current_device() if nccl else "cpu")
+    vec = x if isinstance(x, (list, tuple)) else [x]
+    t = torch.tensor(vec, dtype=torch.float64, device=torch.cuda.current_device() if nccl else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    out = [float(v) for v in t.tolist()]
+    return out if isinstance(x, (list, tuple)) else out[0]
+
+
+def step_stats(ms):
+    return {"median": statistics.median(ms), "min": min(ms), "max": max(ms), "n": len(ms)}
 
 
 class ClockSampler:
@@ -132,7 +199,7 @@ class ClockSampler:
             for k, n in enumerate(names):
                 if len(r) > 4 + k and r[4 + k].lower() == "active":
                     reasons.add(n)
-        num = lambda k: [float(r[k]) for r in self.rows if len(r) > k and r[k].replace(".", "").isdigit()]
+        num = lambda k: [float(r[k]) for r in self.rows if len(r) > k and r[k].replace(".", "").isdigit()]  # noqa: E731
         mem, mem_max = num(8), num(9)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(sm),
@@ -144,6 +211,19 @@ def peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def host_description() -> dict:
+    """the host cores the oracle runs on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cores": len(os.sched_getaffinity(0))}
 
 
 def ncu_traffic(mode, bytes_per_launch, key="traffic_over_algorithmic"):
@@ -161,9 +241,9 @@ def ncu_traffic(mode, bytes_per_launch, key="traffic_over_algorithmic"):
     return cap[key] * bytes_per_launch, os.path.relpath(hits[-1], ROOT)
 
 
-def arm_config(args, world, parts, payload_bytes, raw_bytes, replicated, extra=None):
+def arm_config(args, config, world, parts, payload_bytes, raw_bytes, replicated, extra=None):
     """The JSON line's `config` -- identical for our arm and the reference arm."""
-    return {"workload": args.config, "mode": args.mode, "fanout": args.fanout, "chunk_mib": args.chunk_mib,
+    return {"workload": config, "mode": args.mode, "fanout": args.fanout, "chunk_mib": args.chunk_mib,
             "engine": args.engine, "streams": args.streams, "ctas": args.ctas, "partitions_per_gpu": parts,
             "payload_bytes_per_gpu": payload_bytes, "raw_bytes_per_gpu": raw_bytes,
             "verify": "fletcher64 per 1 MiB block, every block",
@@ -172,73 +252,198 @@ def arm_config(args, world, parts, payload_bytes, raw_bytes, replicated, extra=N
             **(extra or {})}
 
 
+# ---------------------------------------------------------------------------------------
+# The oracle leg (cpu_baseline of our arm, and the whole reference arm).  ONE protocol for
+# both: the first `budget` bytes of each sampled partition (whole tensors), converted by the
+# oracle's converter into fresh NumPy memory, then oracle.loader.load_sample (parse the
+# index, copy every tensor, recompute + compare every 1 MiB Fletcher-64 block) timed per
+# rep.  Mode (i): one process = 1 core.  Mode (ii): P = min(#partitions,
+# usable cores) processes, one partition sample each, started together per rep; aggregate =
+# all payload / (last end - first start).
+# ---------------------------------------------------------------------------------------
+def _oracle_sample_inputs(config: str, part: int, budget: int):
+    import numpy as np
+    from oracle import index as oindex, layout as olayout
+    from synth import models, payload
+    inv, seed = models.model_inventory(config)
+    lay = olayout.plan([(t.name, t.device, t.dtype, t.shape, t.nbytes) for t in inv], 4096, 1 << 20)
+    d = lay.devices()[part]
+    ents = [(i, e) for i, e in enumerate(lay.entries) if e.device == d]
+    first_end = min(e.offset + e.size for _, e in ents)
+    budget = max(budget, -(-first_end // (1 << 20)) << 20)       # at least one whole tensor
+    keep = [i for i, e in ents if e.offset + e.size <= budget]
+    arrs = [np.empty(inv[i].nbytes, np.uint8) for i in keep]      # the seeded payloads (O10)
+    payload.payload_into([a.ctypes.data for a in arrs], [a.size for a in arrs], seed, keep)
+    tensors = [(inv[i].name, d, inv[i].dtype, inv[i].shape, a) for i, a in zip(keep, arrs)]
+    slay, sparts = olayout.convert(tensors, 4096, 1 << 20, config)
+    return oindex.write(slay), sparts, budget
+
+
+def _oracle_worker(config, parts, budget, reps, barrier, q):
+    try:
+        from oracle import loader as oloader
+        inputs = [_oracle_sample_inputs(config, p, budget) for p in parts]
+        spans = []
+        got = 0
+        for _ in range(reps):
+            if barrier is not None:
+                barrier.wait()
+            t0 = time.perf_counter()  # CLOCK_MONOTONIC: comparable across processes
+            got = sum(oloader.load_sample(blob, sp, b) for blob, sp, b in inputs)
+            spans.append((t0, time.perf_counter()))
+        q.put(("ok", got, spans))
+    except Exception as ex:  # noqa: BLE001
+        import traceback
+        q.put(("error", repr(ex), traceback.format_exc()))
+
+
+def oracle_run(config: str, parts, budget: int, reps: int) -> dict:
+    """Time the oracle on samples of `parts` (mode (i) for one partition, mode (ii) for
+    several).  Returns per-rep aggregate seconds and the payload per rep."""
+    import multiprocessing as mp
+    parts = list(parts)
+    cores = len(os.sched_getaffinity(0))
+    P = max(1, min(len(parts), cores))
+    if P == 1:
+        import queue
+        q = queue.Queue()
+        _oracle_worker(config, parts, budget, reps, None, q)
+        res = [q.get()]
+    else:
+        ctx = mp.get_context("spawn")
+        q, barrier = ctx.Queue(), ctx.Barrier(P)
+        groups = [parts[i::P] for i in range(P)]
+        procs = [ctx.Process(target=_oracle_worker, args=(config, g, budget, reps, barrier, q)) for g in groups]
+        for p in procs:
+            p.start()
+        res = [q.get(timeout=3600) for _ in procs]
+        for p in procs:
+            p.join(timeout=60)
+    for r in res:
+        if r[0] != "ok":
+            raise RuntimeError(f"oracle worker failed: {r[1]}\n{r[2]}")
+    got = sum(r[1] for r in res)
+    secs = [max(r[2][k][1] for r in res) - min(r[2][k][0] for r in res) for k in range(reps)]
+    return {"payload": got, "secs": secs, "cores": P, "partitions": len(parts)}
+
+
+def oracle_line_fields(run: dict, budget: int, config: str, timed_reps) -> dict:
+    secs = run["secs"][-timed_reps:] if timed_reps else run["secs"]
+    med = statistics.median(secs)
+    return {"value": run["payload"] / med / 1e9, "unit": "GB/s", "cores": run["cores"], "kind": "oracle",
+            "mode": "(i) 1 process" if run["cores"] == 1 else f"(ii) {run['cores']} processes, one partition each",
+            "median_s": med, "min_s": min(secs), "best_GBps": run["payload"] / min(secs) / 1e9, "reps": len(secs),
+            "sample": f"first {budget / 2**30:.2f} GiB (whole tensors) of each of {run['partitions']} partition(s) of "
+                      f"{config}: {run['payload']} payload bytes per rep -- parse index, copy every tensor, "
+                      f"recompute + compare every 1 MiB Fletcher-64 block (oracle/loader.py load_sample); inputs "
+                      f"built by the oracle converter in fresh NumPy memory, untimed",
+            "host": host_description()}
+
+
+def oracle_budget(args) -> int:
+    """Per-partition sample: --cpu-sample-gib, shrunk for the reference arm so that warm-up +
+    timed steps stay within ~60 GB of oracle work per process (a few minutes)."""
+    b = int(args.cpu_sample_gib * (1 << 30))
+    if args.impl == "reference":
+        b = min(b, max(256 << 20, int(60e9 / max(1, args.warmup + args.steps))))
+    return b
+
+
 def run_reference(args, rank, world):
     """Reference arm = the CPU oracle as it stands (oracle/loader.py) on this box's host
-    cores, each step a bounded sample of the same workload."""
+    cores, each step one bounded sample of the same workload (rank 0 only under torchrun)."""
     if rank != 0:
         return
-    import numpy as np
-    from oracle import index as oindex, layout as olayout, loader as oloader
-    from synth import models, payload
-
-    inv, seed = models.model_inventory(args.config)
-    # per-step sample: --cpu-sample-gib, shrunk so that warmup + steps stay within ~60 GB of
-    # oracle work (~2 minutes on one core) whatever K and W the driver passes
-    budget = int(min(args.cpu_sample_gib * (1 << 30), max(256 << 20, 60e9 / max(1, args.warmup + args.steps))))
-    # oracle converter over the sample's tensors (prefix of partition 0 in source order)
+    from oracle import layout as olayout
+    from synth import models
+    config = resolve_config(args, world)
+    inv, _ = models.model_inventory(config)
     lay = olayout.plan([(t.name, t.device, t.dtype, t.shape, t.nbytes) for t in inv], 4096, 1 << 20)
-    d0 = lay.devices()[0]
-    first = min((e for e in lay.entries if e.device == d0), key=lambda e: e.offset)
-    budget = max(budget, -(-(first.offset + first.size) // (1 << 20)) << 20)  # at least one whole tensor
-    keep = [i for i, e in enumerate(lay.entries) if e.device == d0 and e.offset + e.size <= budget]
-    sub = [inv[i] for i in keep]
-    tensors = [(t.name, t.device, t.dtype, t.shape, payload.payload_bytes(seed, keep[k], t.nbytes))
-               for k, t in enumerate(sub)]
-    slay, sparts = olayout.convert(tensors, 4096, 1 << 20, args.config)
-    blob = oindex.write(slay)
-    times, got = [], 0
-    for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        got = oloader.load_sample(blob, sparts, budget)
-        dt = time.perf_counter() - t0
-        if s >= args.warmup:
-            times.append(dt)
-    T = sum(times)
-    v = got * args.steps / T / 1e9
     n_parts = len(lay.devices())
-    sel = list(range(n_parts)) if args.all_partitions else [0]
+    replicated = args.fanout != "none"
+    # the partitions our arm loads per node: all of a sharded config across its ranks (each
+    # rank one), partition 0 of a replicated or single-GPU run
+    if args.all_partitions:
+        sel = list(range(n_parts))
+    elif replicated or n_parts == 1:
+        sel = [0]
+    else:
+        sel = sorted({r % n_parts for r in range(world)})
+    budget = oracle_budget(args)
+    run = oracle_run(config, sel, budget, args.warmup + args.steps)
+    cpu = oracle_line_fields(run, budget, config, args.steps)
+    T = sum(run["secs"][args.warmup:])
+    v = run["payload"] * args.steps / T / 1e9
+    cpu["value"] = v
     devs = [lay.devices()[p] for p in sel]
-    ref_config = arm_config(args, world, len(sel), sum(e.size for e in lay.entries if e.device in devs),
-                            sum(lay.partitions[d] for d in devs), args.fanout != "none")
+    per_gpu = sel[:1] if not args.all_partitions else sel
+    pdevs = [lay.devices()[p] for p in per_gpu]
     line = {"metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": T / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "impl": "reference",
-            "config": ref_config,
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": f"parse index + copy + verify {got} B of {args.config} partition 0"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic", "impl": "reference",
+            "config": arm_config(args, config, world, len(per_gpu), sum(e.size for e in lay.entries if e.device in pdevs),
+                                 sum(lay.partitions[d] for d in pdevs), replicated),
+            "step_s": step_stats(run["secs"][args.warmup:]),
+            "cpu_baseline": cpu,
+            "sampled_partitions": [int(d) for d in devs],
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args, bufs, idx, inv, seed):
-    """The oracle as it stands, single process (1 core), on a bounded sample of the same
-    pinned partition: parse index, copy tensors, recompute and compare checksums."""
-    from oracle import loader as oloader
-    budget = int(args.cpu_sample_gib * (1 << 30))
-    p0 = sorted(bufs)[0]
-    first = min((t for t in idx.tensors if t.partition == p0), key=lambda t: t.offset)
-    budget = max(budget, -(-(first.offset + first.nbytes) // (1 << 20)) << 20)  # at least one whole tensor
-    blob = idx.serialize()
-    src = {idx.partitions[p].device: bufs[p].numpy() for p in bufs}
-    t0 = time.perf_counter()
-    got = oloader.load_sample(blob, src, budget)
-    dt = time.perf_counter() - t0
-    return {"value": got / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"{got} payload bytes ({args.cpu_sample_gib} GiB budget) of partition 0: parse index, "
-                      f"copy every tensor, recompute+compare 1 MiB Fletcher-64 blocks; {dt:.1f} s"}
+# ---------------------------------------------------------------------------------------
+# Plumbing dry run (CPU, gloo): the launcher, rank -> partition selection, barriers and
+# max-over-ranks timing, with a host memcpy of each rank's partition standing in for the
+# load.  Not a measurement; tests/test_bench_launch.py drives it.
+# ---------------------------------------------------------------------------------------
+def run_plumbing(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from synth import models
+    config = resolve_config(args, world)
+    inv, _ = models.model_inventory(config)
+    devs = sorted({t.device for t in inv})
+    sel = choose_partitions(args, rank, world, len(devs), args.fanout != "none")
+    nbytes = min(sum(t.nbytes for t in inv if t.device == devs[sel[0]]), 64 << 20)
+    src = np.random.default_rng(rank).integers(0, 256, nbytes, dtype=np.uint8)
+    dst = np.empty_like(src)
+    if world > 1:
+        dist.barrier()
+    secs = []
+    for _ in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        dst[:] = src
+        secs.append(time.perf_counter() - t0)
+    secs = max_over_ranks(secs[args.warmup:], world)
+    ranks = [None] * world
+    mine = {"rank": rank, "local_rank": local, "pid": os.getpid(), "partitions": sel,
+            "world_size_env": int(os.environ.get("WORLD_SIZE", 1))}
+    if world > 1:
+        dist.all_gather_object(ranks, mine)
+    else:
+        ranks = [mine]
+    if rank == 0:
+        T = sum(secs)
+        print(json.dumps({"metric": METRIC, "value": nbytes * world * args.steps / T / 1e9, "unit": "GB/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": T / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                          "plumbing": True, "config": {"workload": config}, "ranks": ranks}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
+def choose_partitions(args, rank, world, n_parts, replicated):
+    if args.all_partitions:
+        return list(range(n_parts))
+    if replicated or n_parts == 1:
+        return [0]
+    return [rank % n_parts]
+
+
+# ---------------------------------------------------------------------------------------
+# Rooflines measured in the same run
+# ---------------------------------------------------------------------------------------
 def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1, gpus=None):
     """B_h2d(N): the copy engine's best host->device rate from the same pinned buffer into
     the same destination over >= 4 GiB: max of one 4 GiB
@@ -278,6 +483,66 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1, gpus=None):
             best = max(best, world * sum(sizes.values()) / (ms * 1e-3) / 1e9)
         out[name] = best
     return max(out.values()), out
+
+
+def nvlink_peaks(torch, world, gpu, mib=1024, reps=3):
+    """NVLink fan-out roofline, measured over the job's NCCL process group
+    in the same run, best of `reps`, barrier-started, max-over-ranks time:
+      bcast_GBps     : ncclBroadcast of `mib` MiB, root rotating (bus bandwidth = algorithm
+                       bandwidth for a broadcast);
+      allgather_busbw: ncclAllGather of mib/N MiB per rank, busbw = (N-1)/N * total / t;
+      p2p_ingress    : every rank sends `mib` MiB to rank+1 and receives from rank-1 at once
+                       (ncclSend/Recv), per-rank ingress rate.
+    A replicated load's NVLink bound is S(N-1)/N per GPU of ingress over these rates."""
+    import torch.distributed as dist
+    dev = torch.device("cuda", gpu) if dist.get_backend() == "nccl" else torch.device("cpu")
+    if dev.type == "cpu":  # gloo plumbing runs (SLLM_BENCH_SAME_GPU): a token size
+        mib = min(mib, 64)
+    n = (mib << 20)
+    buf = torch.empty(n, dtype=torch.uint8, device=dev)
+    rbuf = torch.empty(n, dtype=torch.uint8, device=dev)
+    per = n // world
+    ag_in = buf[:per]
+    ag_out = [rbuf[q * per:(q + 1) * per] for q in range(world)]
+    rank = dist.get_rank()
+
+    def timed(fn):
+        best = None
+        for _ in range(reps):
+            dist.barrier()
+            if dev.type == "cuda":
+                torch.cuda.synchronize(gpu)
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                fn()
+                e.record()
+                e.synchronize()
+                ms = s.elapsed_time(e)
+            else:
+                t0 = time.perf_counter()
+                fn()
+                ms = (time.perf_counter() - t0) * 1e3
+            ms = max_over_ranks(ms, world)
+            best = ms if best is None else min(best, ms)
+        return best
+
+    k = [0]
+
+    def bcast():
+        dist.broadcast(buf, src=k[0] % world)
+        k[0] += 1
+
+    def p2p():
+        ops = [dist.P2POp(dist.isend, buf, (rank + 1) % world), dist.P2POp(dist.irecv, rbuf, (rank - 1) % world)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+    t_b = timed(bcast)
+    t_ag = timed(lambda: dist.all_gather(ag_out, ag_in))
+    t_p = timed(p2p)
+    return {"bcast_GBps": n / (t_b * 1e-3) / 1e9,
+            "allgather_busbw_GBps": (world - 1) / world * per * world / (t_ag * 1e-3) / 1e9,
+            "p2p_ingress_GBps": n / (t_p * 1e-3) / 1e9, "bytes": n, "backend": dist.get_backend()}
 
 
 def standalone_hbm(idx, bufs, torch, sllm, reps=5):
@@ -321,26 +586,71 @@ def standalone_hbm(idx, bufs, torch, sllm, reps=5):
     return res
 
 
-def main():
-    args = parse()
+def replicated_baselines(sllm, torch, idx, bufs, gpus, cfg, bases, world, rank, reps=2):
+    """the replicated load without the fan-out, at the same N, same buffers.
+      naive      : every rank loads the whole partition over its own PCIe link (N*S PCIe bytes);
+      root_bcast : rank 0 loads S, then one NCCL broadcast of S to every rank (S over one link).
+    Aggregate GB/s = N full replicas / max-over-ranks device time, best of `reps`."""
+    import torch.distributed as dist
+    from dataclasses import replace
+    p = 0
+    S = idx.partitions[p].length
+    payload = sum(t.nbytes for t in idx.tensors if t.partition == p)
+    nc = replace(cfg, fanout="none", profile=False)
+    st = torch.cuda.current_stream(gpus[p])
+    out = {}
+    for name in ("naive", "root_bcast"):
+        best = None
+        for _ in range(reps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(st)
+            if name == "naive" or rank == 0:
+                res = sllm.load_start(idx, {p: bufs[p]}, {p: gpus[p]}, nc, bases, None, {p: st}, None)
+                res.wait()
+                del res
+            if name == "root_bcast" and world > 1:
+                dist.broadcast(bases[p], src=0)
+            e.record(st)
+            e.synchronize()
+            ms = max_over_ranks(s.elapsed_time(e), world)
+            best = ms if best is None else min(best, ms)
+        out[name] = {"value": payload * world / (best * 1e-3) / 1e9, "unit": "GB/s", "ms": best,
+                     "pcie_bytes_total": S * (world if name == "naive" else 1)}
+    return out
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    maybe_self_launch(args, argv)
     rank, world, local = dist_env()
+    if world > 1 and args.gpus not in (1, world):
+        fail_loudly(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "reference":
+        run_reference(args, rank, world)  # rank 0 alone (no process group: the others exit at once)
+        return
+    if args.plumbing:
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_plumbing(args, rank, world, local)
+        return
+    import torch
     if world > 1:
         import torch.distributed as dist
-        import torch
+        if not SAME_GPU and visible_gpus() < world:
+            fail_loudly(f"{world} ranks need {world} visible GPUs, found {visible_gpus()}")
         torch.cuda.set_device(gpu_of(local))
         if SAME_GPU:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+    elif not torch.cuda.is_available():
+        fail_loudly("no CUDA GPU visible (bench.py measures the GPU path; --plumbing for a CPU dry run)")
 
-    import torch
     import paper_2401_14351_b200 as sllm
     from paper_2401_14351_b200 import workloads
     from synth import models, payload
@@ -349,23 +659,21 @@ def main():
     gpu = gpu_of(local)
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
+    config = resolve_config(args, world)
 
     # ---- setup (untimed): synthetic checkpoint packed into pinned DRAM by the converter
     t0 = time.perf_counter()
-    inv, seed = models.model_inventory(args.config)
+    inv, seed = models.model_inventory(config)
     replicated = args.fanout != "none"
     if replicated and len(set(t.device for t in inv)) != 1:
         raise SystemExit("--fanout needs a single-partition (replicated) checkpoint config")
     n_parts = len(set(t.device for t in inv))
-    if args.all_partitions:
-        sel = list(range(n_parts))
-    else:
-        sel = [0] if world == 1 or n_parts == 1 else [rank]
+    sel = choose_partitions(args, rank, world, n_parts, replicated)
     if args.spread and (not args.all_partitions or world > 1 or replicated):
         raise SystemExit("--spread goes with --all-partitions in a single process (no fan-out)")
     ndev = torch.cuda.device_count() if args.spread else 1
     gpu_map = {p: (p % ndev if args.spread else gpu) for p in sel}
-    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=sel, gpu_of=gpu_map)
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, config, partitions=sel, gpu_of=gpu_map)
     t_setup = time.perf_counter() - t0
     blob = idx.serialize()
     parts = sorted(bufs)
@@ -386,10 +694,13 @@ def main():
     payload_bytes = sum(t.nbytes for t in idx.tensors if t.partition in bufs)
     raw_bytes = sum(idx.partitions[p].length for p in parts)
 
-    b_h2d, b_h2d_methods = h2d_peak(bufs, bases if not cfg.scatter else {p: torch.empty(min(4 << 30, idx.partitions[p].length),
-                                                                          dtype=torch.uint8, device=f"cuda:{gpus[p]}") for p in parts},
-                     torch, world=world, gpus=gpus)
-    stream = torch.cuda.current_stream(gpu)
+    peak_dst = bases if not cfg.scatter else {
+        p: torch.empty(min(4 << 30, idx.partitions[p].length), dtype=torch.uint8, device=f"cuda:{gpus[p]}") for p in parts}
+    b_h2d, b_h2d_methods = h2d_peak(bufs, peak_dst, torch, world=world, gpus=gpus)
+    del peak_dst
+    nvl = None
+    if replicated and world > 1:
+        nvl = nvlink_peaks(torch, world, gpu)
     streams = {p: torch.cuda.current_stream(gpus[p]) for p in parts}
     comm = None
     if args.fanout == "p2p":      # peer group bound to every rank's replica (CUDA IPC over the process group)
@@ -417,21 +728,24 @@ def main():
     sync_all()
     reports = []
     with ClockSampler(gpu) as clk:
-        # one start/end pair per GPU this process loads (its caller stream is gated on the
-        # load); the step time is the slowest GPU's
-        marks = {g: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for g in used}
-        for g in used:
-            marks[g][0].record(torch.cuda.current_stream(g))
-        for _ in range(args.steps):
+        # per-step start/end events on every GPU this process loads (its caller stream is
+        # gated on the load); a step's time is its slowest GPU's, the run's the sum
+        marks = [{g: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for g in used}
+                 for _ in range(args.steps)]
+        for k in range(args.steps):
+            for g in used:
+                marks[k][g][0].record(torch.cuda.current_stream(g))
             res, ix = step(not args.no_profile)
             reports.append(res.wait())
+            for g in used:
+                marks[k][g][1].record(torch.cuda.current_stream(g))
             del res, ix
-        for g in used:
-            marks[g][1].record(torch.cuda.current_stream(g))
         sync_all()
     if world > 1:
         dist.barrier()
-    ms_total = max_over_ranks(max(a.elapsed_time(b) for a, b in marks.values()), world)
+    first_last = max(marks[0][g][0].elapsed_time(marks[-1][g][1]) for g in used)
+    ms_total = max_over_ranks(first_last, world)
+    ms_steps = max_over_ranks([max(m[g][0].elapsed_time(m[g][1]) for g in used) for m in marks], world)
     ms_step = ms_total / args.steps
     # every rank ends the step with its own loaded model (sharded: its partition; replicated:
     # a full replica, of which it moved 1/N over PCIe)
@@ -446,13 +760,15 @@ def main():
     e2e_t = []
     for _ in range(2):
         sync_all()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         ix = sllm.Index.from_bytes(blob)
         if comm is None:
             res = sllm.load(ix, bufs, gpus, sllm.LoadConfig(**{**cfg.__dict__, "profile": False}))
         else:  # a replicated group is bound to its replicas: no per-step allocation
             res = sllm.load_start(ix, bufs, gpus, sllm.LoadConfig(**{**cfg.__dict__, "profile": False}), bases,
-                                  per_tensor, {p: stream for p in parts}, comm)
+                                  per_tensor, streams, comm)
             res.wait()
         sync_all()
         e2e_t.append(time.perf_counter() - t0)
@@ -465,6 +781,10 @@ def main():
                         if comm is not None else "torch allocation + index open + load + verify + wait"),
            "time_to_loaded_model_s": t_e2e}
 
+    baselines = None
+    if replicated and not args.no_baselines:
+        baselines = replicated_baselines(sllm, torch, idx, bufs, gpus, cfg, bases, world, rank)
+
     # ---- roofline of the dominant kernel, from the library's per-launch CUDA events
     rep = reports[-1]
     kern_ms = sum(r["t_kernel_ms_sum"] for r in reports) / len(reports)
@@ -473,9 +793,9 @@ def main():
     roof = None
     pcie_rate = pcie_bytes * world / (ms_step * 1e-3) / 1e9
     h2d = {"bound": "pcie", "achieved": pcie_rate, "peak": b_h2d, "unit": "GB/s",
-           "frac": pcie_rate / b_h2d, "peak_methods": b_h2d_methods, "n_links": world,
+           "frac": pcie_rate / b_h2d, "peak_methods": b_h2d_methods, "n_links": world * len(used),
            "what": "host->device bytes of the whole step (a1-a8) over its device time vs the copy engine's "
-                   "measured host->device peak on the same buffers (all links at once under torchrun)"}
+                   "measured host->device peak on the same buffers (all links at once, barrier-started)"}
     if args.mode in ("ce", "scatter_ce") and kern_launches and kern_ms > 0:
         # the step's kernel: K4 (CE) / K3 (SCATTER_CE) on each landed chunk, per-launch
         # CUDA events recorded by the library on its kernel stream over the timed region
@@ -498,15 +818,26 @@ def main():
         # over the step's device time (the kernel is the only work in the step).
         achieved = kern_bytes / (ms_step * 1e-3) / 1e9
         traffic, traffic_src = ncu_traffic(args.mode, kern_bytes / kern_launches, key="sysmem_over_algorithmic")
-        roof = {"bound": "pcie", "achieved": achieved, "peak": b_h2d / world, "unit": "GB/s",
-                "frac": achieved / (b_h2d / world), "traffic": traffic, "traffic_source": traffic_src,
+        per_link = b_h2d / (world * len(used))
+        roof = {"bound": "pcie", "achieved": achieved, "peak": per_link, "unit": "GB/s",
+                "frac": achieved / per_link, "traffic": traffic, "traffic_source": traffic_src,
                 "traffic_note": "bytes the launch pulled from host memory over PCIe (ncu syslts sysmem sectors x 32) "
                                 "-- the bounding link; its HBM writes mostly stay in the 126 MB L2 past the launch",
                 "kernel": "materialise_tma_kernel<store,check> (zero-copy host source)",
                 "launches_per_step": kern_launches, "avg_launch_ms": kern_ms / max(kern_launches, 1),
-                "peak_source": "cudaMemcpyAsync H2D from the same pinned buffer, 4 GiB, best of 5, this run"}
+                "peak_source": "cudaMemcpyAsync H2D from the same pinned buffer, 4 GiB, best of 3, this run"}
+    nvlink = None
+    if nvl is not None:
+        # each GPU receives S(N-1)/N over NVLink per load; its rate against the measured
+        # collective rates of the same group
+        ingress = (idx.partitions[0].length - pcie_bytes) / (ms_step * 1e-3) / 1e9
+        ref = {"bcast": nvl["bcast_GBps"], "allgather": nvl["allgather_busbw_GBps"],
+               "p2p": nvl["p2p_ingress_GBps"]}[args.fanout]
+        nvlink = {"bound": "nvlink", "achieved": ingress, "peak": ref, "unit": "GB/s", "frac": ingress / ref,
+                  "what": "per-GPU NVLink ingress of the fan-out (S(N-1)/N per load) over its device time vs the "
+                          "measured rate of the matching collective on the same group", "measured": nvl}
     standalone = None
-    if not args.no_standalone and rank == 0:
+    if not args.no_standalone and rank == 0 and not replicated:
         bases = per_tensor = None
         torch.cuda.empty_cache()
         standalone = standalone_hbm(idx, bufs, torch, sllm)
@@ -519,22 +850,26 @@ def main():
             roof = {"bound": "hbm", "achieved": k4["GBps"], "peak": hbm, "unit": "GB/s", "frac": k4["GBps"] / hbm,
                     "traffic": None, "kernel": "materialise_kernel<checksum only> (K4, standalone 4 GiB)"}
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, bufs, idx, inv, seed)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        budget = oracle_budget(args)
+        run = oracle_run(config, parts, budget, args.cpu_reps)
+        cpu = oracle_line_fields(run, budget, config, None)
     clocks = clk.summary()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": arm_config(args, world, len(parts), payload_bytes, raw_bytes, replicated, {
+                "config": arm_config(args, config, world, len(parts), payload_bytes, raw_bytes, replicated, {
                     **({"spread": f"{len(parts)} partitions over GPUs {used} from one process"} if args.spread else {}),
                     **({"same_gpu_plumbing_check": "all ranks on cuda:0 (gloo); not a scaling number"}
                        if SAME_GPU and world > 1 else {})}),
-                "time_to_loaded_model_s": ms_step * 1e-3, "t_alloc_s": t_alloc, "t_setup_s": t_setup,
+                "time_to_loaded_model_s": ms_step * 1e-3, "step_ms": step_stats(ms_steps),
+                "t_alloc_s": t_alloc, "t_setup_s": t_setup,
                 "b_h2d_measured_GBps": b_h2d, "frac_h2d": pcie_rate / b_h2d,
                 "gpu_launches": int(rep["kernel_launches"]) * args.steps,
                 "copy_calls_per_step": int(rep["copy_calls"]),
-                "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_h2d": h2d, "standalone_hbm": standalone,
+                "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_h2d": h2d, "roofline_nvlink": nvlink,
+                "replicated_baselines": baselines, "standalone_hbm": standalone,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if comm is not None:

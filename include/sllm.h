@@ -184,6 +184,13 @@ SLLM_API sllm_status sllm_replica_slices(uint64_t length, uint64_t chunk, int32_
  * SLLM_E_LOOKUP if round >= n_rounds. */
 SLLM_API sllm_status sllm_replica_round(uint64_t length, uint64_t chunk, int32_t nranks, uint64_t round,
                                         uint64_t* lo_hi, uint64_t* n_rounds);
+/* Unit of the NCCL fan-outs' slices and rounds for a load with chunk size `chunk` and fan-out
+ * `fanout`: BCAST / ALLGATHER slice the partition and run their rounds in whole copy windows
+ * of chunks (max(1, 64 MiB / chunk) chunks -- one batched copy submission and one grouped
+ * broadcast / all-gather per round instead of one per chunk); every other fan-out: `chunk`.
+ * The loader calls sllm_replica_slices / sllm_replica_round / sllm_allgather_round with this
+ * unit in place of the chunk. */
+SLLM_API sllm_status sllm_fanout_unit(uint64_t chunk, int32_t fanout, uint64_t* unit);
 /* All-gather schedule of SLLM_FANOUT_ALLGATHER ("in-place ncclAllGather is the
  * equal-count alternative"): chunk k of the partition belongs to rank k mod nranks, so
  * round r is the contiguous run of chunks [r*nranks, (r+1)*nranks) and rank q contributes

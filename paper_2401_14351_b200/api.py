@@ -220,6 +220,14 @@ def replica_slices(length: int, chunk: int, nranks: int) -> List[Tuple[int, int]
     return [(arr[2 * r], arr[2 * r + 1]) for r in range(nranks)]
 
 
+def fanout_unit(chunk: int, fanout: str) -> int:
+    """sllm_fanout_unit: the slice / round unit a load with this chunk size and fan-out uses
+    (NCCL fan-outs: a whole >= 64 MiB window of chunks)."""
+    out = C.c_uint64()
+    check(lib().sllm_fanout_unit(chunk, {"none": 0, "bcast": 1, "p2p": 2, "allgather": 3}[fanout], C.byref(out)))
+    return out.value
+
+
 def replica_schedule(length: int, chunk: int, nranks: int) -> List[List[Tuple[int, int]]]:
     """The fan-out rounds the replicated load executes: rounds[r][q] = (lo, hi) that rank
     q broadcasts in round r (lo == hi: nothing)."""

@@ -29,6 +29,9 @@ void sllm_load_tensor_internal(const sllm_load*, const char*, sllm_tensor_handle
 void sllm_load_block_checksums_internal(sllm_load*, size_t, const uint64_t**);
 void sllm_load_free_internal(sllm_load*);
 void sllm_device_trim_internal(int32_t gpu, uint64_t keep_bytes);
+namespace sllm {
+uint64_t fanout_unit(uint64_t chunk, int32_t fanout);
+}
 void sllm_comm_unique_id_internal(void*);
 sllm_comm* sllm_comm_init_rank_internal(const void*, int32_t, int32_t, int32_t);
 void sllm_comm_init_all_internal(const int32_t*, int32_t, sllm_comm**);
@@ -294,6 +297,13 @@ sllm_status sllm_allgather_round(uint64_t length, uint64_t chunk, int32_t nranks
       all = all && b - a == chunk;
     }
     if (full) *full = all ? 1 : 0;
+  });
+}
+
+sllm_status sllm_fanout_unit(uint64_t chunk, int32_t fanout, uint64_t* unit) {
+  return guard([&] {
+    if (!chunk || !unit) fail(SLLM_E_INVALID, "bad fan-out unit arguments");
+    *unit = fanout_unit(chunk, fanout);
   });
 }
 

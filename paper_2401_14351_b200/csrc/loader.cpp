@@ -324,6 +324,15 @@ static void copy_window(PartJob& j, int prof, uint8_t* dst, const uint8_t* wsrc,
   timed_end(e, j.cev, xs);
 }
 
+// Unit of the NCCL fan-outs' slicing and rounds: a whole copy window (>= kWindowBytes of
+// chunks), so every round is one batched copy submission and one grouped broadcast /
+// all-gather per root instead of one per chunk; the chunk stays the copy engine's
+// transfer unit inside it.  The P2P fan-out and unreplicated loads slice by chunk.
+uint64_t fanout_unit(uint64_t chunk, int32_t fanout) {
+  if (fanout != SLLM_FANOUT_BCAST && fanout != SLLM_FANOUT_ALLGATHER) return chunk;
+  return std::max<uint64_t>(1, kWindowBytes / chunk) * chunk;
+}
+
 // Largest verification span (kVerifyBytes; SLLM_VERIFY_SPAN_MIB: measurement knob).
 static uint64_t verify_span_bytes() {
   static const uint64_t v = [] {
@@ -487,7 +496,8 @@ static void run_job(sllm_load* L, PartJob& j) {
     if (atoll(e) > 0 && !files) scatter_win = (uint64_t)atoll(e) << 20;
   const uint64_t win_bytes = cfg.mode == SLLM_MODE_SCATTER_CE ? scatter_win : kWindowBytes;
   const bool nccl_fanout = cfg.fanout == SLLM_FANOUT_BCAST || cfg.fanout == SLLM_FANOUT_ALLGATHER;
-  P.window = nccl_fanout ? 1 : std::max<uint64_t>(1, win_bytes / cfg.chunk_bytes);
+  P.window = nccl_fanout ? fanout_unit(cfg.chunk_bytes, cfg.fanout) / cfg.chunk_bytes
+                         : std::max<uint64_t>(1, win_bytes / cfg.chunk_bytes);
   const uint64_t nch_all = std::max<uint64_t>(1, ceil_div(pr.length, cfg.chunk_bytes));
   if (cfg.mode == SLLM_MODE_SCATTER_CE && !files) {
     // windows of P.window chunks, halving over the last two windows' worth of chunks down
@@ -576,9 +586,10 @@ static void run_job(sllm_load* L, PartJob& j) {
     std::vector<uint64_t> lohi(2 * R);
     uint64_t rounds = 0;
     int32_t full = 0;
+    const uint64_t U = fanout_unit(C, cfg.fanout);  // round unit: a whole window of chunks
     auto schedule = [&](uint64_t r, uint64_t* n) {
-      return ag ? sllm_allgather_round(pr.length, C, R, r, lohi.data(), n, &full)
-                : sllm_replica_round(pr.length, C, R, r, lohi.data(), n);
+      return ag ? sllm_allgather_round(pr.length, U, R, r, lohi.data(), n, &full)
+                : sllm_replica_round(pr.length, U, R, r, lohi.data(), n);
     };
     if (schedule(0, &rounds) != SLLM_OK && pr.length) fail(SLLM_E_INVALID, "fan-out schedule failed");
     cudaEvent_t evk;
@@ -601,7 +612,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       sp[0].end = pr.length;
     } else {
       std::vector<uint64_t> sl(2 * R);
-      if (sllm_replica_slices(pr.length, C, R, sl.data()) != SLLM_OK) fail(SLLM_E_INVALID, "bad slices");
+      if (sllm_replica_slices(pr.length, U, R, sl.data()) != SLLM_OK) fail(SLLM_E_INVALID, "bad slices");
       for (int q = 0; q < R; ++q) sp[q].end = sl[2 * q + 1];
     }
     auto extend = [&](Span& v, uint64_t a, uint64_t b) {
@@ -619,16 +630,16 @@ static void run_job(sllm_load* L, PartJob& j) {
       if (schedule(r, nullptr) != SLLM_OK) fail(SLLM_E_INVALID, "fan-out schedule failed");
       std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
       for (int q = 0; q < R; ++q) ranges[q] = {lohi[2 * q], lohi[2 * q + 1]};
-      if (ranges[me].second > ranges[me].first) {  // this rank's own chunk of the round: PCIe
-        const uint64_t lo = ranges[me].first;
-        cudaStream_t done = issue_window(idx, cfg_own, j, P, r, lo / C, lo / C + 1, true);
+      if (ranges[me].second > ranges[me].first) {  // this rank's own unit of the round: PCIe
+        const uint64_t lo = ranges[me].first, hi = ranges[me].second;
+        cudaStream_t done = issue_window(idx, cfg_own, j, P, r, lo / C, ceil_div(hi, C), true);
         SLLM_CUDA(cudaEventRecord(evk, done));
         SLLM_CUDA(cudaStreamWaitEvent(cs, evk, 0));
       }
       for (int q = 0; q < R; ++q)
         if (q != me && ranges[q].second > ranges[q].first) j.fanout += ranges[q].second - ranges[q].first;
       if (ag && full) {  // NVLink: one in-place all-gather of the round's R whole chunks
-        nccl_allgather_inplace(L->comm, ranges[0].first, C, j.dst_base, cs);
+        nccl_allgather_inplace(L->comm, ranges[0].first, U, j.dst_base, cs);
       } else {
         nccl_bcast_group(L->comm, ranges, j.dst_base, cs);  // NVLink: every root's chunk to every rank
       }
@@ -875,11 +886,12 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
     if (cfg.fanout != SLLM_FANOUT_NONE) {  // this rank's slice: the only bytes it reads from the host
       const int R = comm_nranks(comm), me = comm_rank(comm);
       std::vector<uint64_t> lohi(2 * R);
-      if (sllm_replica_slices(j.hi, cfg.chunk_bytes, R, lohi.data()) != SLLM_OK) fail(SLLM_E_INVALID, "bad slices");
+      const uint64_t U = fanout_unit(cfg.chunk_bytes, cfg.fanout);
+      if (sllm_replica_slices(j.hi, U, R, lohi.data()) != SLLM_OK) fail(SLLM_E_INVALID, "bad slices");
       j.lo = lohi[2 * me];
       j.hi = lohi[2 * me + 1];
-      if (cfg.fanout == SLLM_FANOUT_ALLGATHER) {  // chunks me, me+R, me+2R, ... (strided)
-        j.lo = std::min((uint64_t)me * cfg.chunk_bytes, idx->parts[p].length);
+      if (cfg.fanout == SLLM_FANOUT_ALLGATHER) {  // units me, me+R, me+2R, ... (strided)
+        j.lo = std::min((uint64_t)me * U, idx->parts[p].length);
         j.hi = idx->parts[p].length;
       }
     }

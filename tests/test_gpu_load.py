@@ -250,19 +250,33 @@ def test_materialise_device_matches_oracle(engine, monkeypatch):
         assert ex.value.status == 9
 
 
-def test_fanout_single_rank_nccl():
-    """The replicated path with one rank exercises NCCL init + grouped broadcasts; the
-    result must equal P_0 exactly (O9(c))."""
-    inv, seed = models.model_inventory("toy")
+@pytest.mark.parametrize("workload", ["toy", "300mb"])
+def test_fanout_single_rank_nccl(workload):
+    """The replicated path with one rank exercises NCCL init + grouped broadcasts / in-place
+    all-gathers; the result must equal P_0 exactly (O9(c)).  Rounds run in whole 64 MiB
+    units of chunks (sllm_fanout_unit): the toy is one ragged round, the ~300 MB replica
+    four full rounds (in-place all-gathers) and a ragged last one."""
+    if workload == "toy":
+        inv, seed = models.model_inventory("toy")
+    else:
+        rng = np.random.default_rng(31)   # 60 tensors of 2.5-7.5 MB with odd shapes (~300 MB)
+        inv, seed = [models.TensorSpec(f"w{i}", 0, "f16", (int(rng.integers(1200, 3700)), 1029))
+                     for i in range(60)], 31
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
     lay, oparts, payloads = oracle_of(inv, seed, 4096, 1 << 20)
+    L = idx.partitions[0].length
     comm = sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, 0)
-    for fanout in ("bcast", "allgather"):  # allgather: 6 full in-place rounds + a ragged last one
+    for fanout in ("bcast", "allgather"):
+        U = sllm.fanout_unit(2 << 20, fanout)
+        if workload != "toy" and fanout == "allgather":
+            rounds = sllm.allgather_schedule(L, U, 1)
+            assert sum(f for f, _ in rounds) >= 4 and not rounds[-1][0]
         for mode in ("ce", "zerocopy"):
             cfg = sllm.LoadConfig(chunk_bytes=2 << 20, mode=mode, fanout=fanout)
             res = sllm.load(idx, bufs, {0: 0}, cfg, comm=comm)
             check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
-            assert res.report["transferred_bytes"] == idx.partitions[0].length
+            assert res.report["transferred_bytes"] == L
+            assert res.report["copy_calls"] <= -(-L // U) + 1 if mode == "ce" else True
     comm.free()
 
 

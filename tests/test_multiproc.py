@@ -239,3 +239,19 @@ def test_allgather_round_errors():
     assert sllm.lib().sllm_allgather_round(10 << 16, 1 << 16, 3, 4, arr, None, None) == _abi.E_LOOKUP
     assert sllm.lib().sllm_allgather_round(10 << 16, 0, 3, 0, arr, None, None) == _abi.E_INVALID
     assert sllm.lib().sllm_allgather_round(10 << 16, 1 << 16, 0, 0, arr, None, None) == _abi.E_INVALID
+
+
+def test_fanout_unit():
+    """The NCCL fan-outs slice and run rounds in whole >= 64 MiB windows of chunks (one
+    batched copy + one grouped collective per round); P2P / none keep the chunk.  The
+    schedule functions replayed above are the ones the loader calls with this unit."""
+    import paper_2401_14351_b200 as sllm
+    M = 1 << 20
+    for C, U in [(1 * M, 64 * M), (16 * M, 64 * M), (64 * M, 64 * M), (3 * M, 63 * M), (128 * M, 128 * M),
+                 (1 << 16, 64 * M)]:
+        assert sllm.fanout_unit(C, "bcast") == U and sllm.fanout_unit(C, "allgather") == U
+        assert sllm.fanout_unit(C, "p2p") == C and sllm.fanout_unit(C, "none") == C
+    # OPT-30B over 8 ranks at 16 MiB chunks: 894 units, 112 rounds instead of 447 per-chunk rounds
+    L = 59_949_969_408
+    U = sllm.fanout_unit(16 * M, "bcast")
+    assert len(sllm.replica_schedule(L, U, 8)) == 112 and len(sllm.replica_schedule(L, 16 * M, 8)) == 447

@@ -94,3 +94,17 @@ def test_every_single_byte_change_detected():
             misses += fletcher.f64_closed(bytes(x)) == ref
         x[i] = orig
     assert misses == 0
+
+
+@pytest.mark.parametrize("nbytes,fill", [(1 << 20, None), ((1 << 20) + 12, None), (3 << 20, None),
+                                         (1 << 20, 0xFFFFFFFE), (1 << 20, 0xFFFFFFFF)])
+def test_closed_form_equals_sequential_at_block_size(nbytes, fill):
+    """block_checksums applies f64_closed to whole 1 MiB blocks (64 of its 4096-word
+    sub-blocks): pin it there against the literal sequential definition, including the
+    largest residue words (0xFFFFFFFE) that maximise every uint64 partial sum and the
+    0xFFFFFFFF == 0 words of the blind spot."""
+    if fill is None:
+        x = np.random.default_rng(nbytes).integers(0, 256, size=nbytes, dtype=np.uint8).tobytes()
+    else:
+        x = np.full(nbytes // 4, fill, dtype="<u4").tobytes()
+    assert fletcher.f64_closed(x) == fletcher.f64_sequential(x)
