@@ -76,14 +76,37 @@ def _ptr_array(ptrs: Iterable[Optional[int]]) -> C.Array:
     return (C.c_void_p * max(len(ptrs), 1))(*[C.c_void_p(int(p)) if p else None for p in ptrs])
 
 
+# Python-side tables derived from an index's content (TensorInfo list, per-partition view
+# plans), shared by every Index parsed from the same bytes: the C parse and validation (a1)
+# still run for every Index, but the per-tensor Python objects are built once per content
+# instead of once per load (a latency-bound load of a 1,120-tensor LoRA adapter otherwise
+# spends ~1 ms per step creating and tearing them down).  Keyed by the index trailer
+# (Fletcher-64 of every preceding byte + total length); bounded LRU.
+_DERIVED: "Dict[bytes, dict]" = {}
+_DERIVED_MAX = 16
+
+
+def _derived_for(key: Optional[bytes]) -> dict:
+    if key is None:
+        return {}
+    d = _DERIVED.pop(key, None)
+    if d is None:
+        d = {}
+        if len(_DERIVED) >= _DERIVED_MAX:
+            _DERIVED.pop(next(iter(_DERIVED)))
+    _DERIVED[key] = d  # most recently used last
+    return d
+
+
 class Index:
     """Owned handle to a parsed or planned index (sllm_index*)."""
 
-    def __init__(self, handle: int, owned: bool = True):
+    def __init__(self, handle: int, owned: bool = True, key: Optional[bytes] = None):
         self._h = C.c_void_p(handle)
         self._owned = owned  # False: borrowed from another owner (e.g. a PinnedCache entry)
-        self._tensors: Optional[List[TensorInfo]] = None
-        self._by_name: Optional[Dict[str, int]] = None
+        self._derived = _derived_for(key)
+        self._tensors: Optional[List[TensorInfo]] = self._derived.get("tensors")
+        self._by_name: Optional[Dict[str, int]] = self._derived.get("by_name")
 
     # -- constructors ------------------------------------------------------------------
     @classmethod
@@ -102,10 +125,10 @@ class Index:
 
     @classmethod
     def from_bytes(cls, blob: bytes) -> "Index":
-        buf = C.create_string_buffer(bytes(blob), len(blob))
+        blob = bytes(blob)
         out = C.c_void_p()
-        check(lib().sllm_index_from_memory(buf, len(blob), C.byref(out)))
-        return cls(out.value)
+        check(lib().sllm_index_from_memory(blob, len(blob), C.byref(out)))
+        return cls(out.value, key=blob[-16:])
 
     def close(self) -> None:
         if self._h and self._h.value:
@@ -163,6 +186,8 @@ class Index:
 
     @property
     def tensors(self) -> List[TensorInfo]:
+        if self._tensors is None and "tensors" in self._derived:  # built by another Index of this content
+            self._tensors, self._by_name = self._derived["tensors"], self._derived["by_name"]
         if self._tensors is None:
             out = []
             for i in range(self.info()["n_tensors"]):
@@ -172,7 +197,37 @@ class Index:
                                       tuple(t.shape[:t.ndim]), t.offset, t.nbytes))
             self._tensors = out
             self._by_name = {t.name: i for i, t in enumerate(out)}
+            self._derived["tensors"], self._derived["by_name"] = self._tensors, self._by_name
         return self._tensors
+
+    def view_plan(self, p: int):
+        """Per dtype of partition p: (dtype, split sizes in elements over the whole partition,
+        [(name, piece index, shape)]) -- tensors as pieces of one typed split of the base,
+        padding as the pieces in between (cached per index content)."""
+        plans = self._derived.setdefault("view_plans", {})
+        if p not in plans:
+            L = self.partitions[p].length
+            by_dt: Dict[str, list] = {}
+            for t in self.tensors:
+                if t.partition == p:
+                    by_dt.setdefault(t.dtype, []).append(t)
+            plan = []
+            for dt, ts in by_dt.items():
+                w = WIDTH[dt]
+                ts.sort(key=lambda t: t.offset)
+                sizes, items, cur = [], [], 0
+                for t in ts:   # offsets are multiples of A >= 16, sizes of the width
+                    o, n = t.offset // w, t.nbytes // w
+                    if o > cur:
+                        sizes.append(o - cur)
+                    items.append((t.name, len(sizes), t.shape))
+                    sizes.append(n)
+                    cur = o + n
+                if L // w > cur:
+                    sizes.append(L // w - cur)
+                plan.append((dt, sizes, items))
+            plans[p] = plan
+        return plans[p]
 
     def find(self, name: str) -> int:
         i = C.c_size_t()
@@ -497,6 +552,27 @@ class LoadResult:
             pass
 
 
+def _views(index: Index, parts, bases, per_tensor, scatter: bool) -> Dict[str, object]:
+    """{name: torch tensor} of a load: scatter -> the caller's per-tensor buffers; contiguous
+    -> zero-copy views base + offset, made with one typed split of each
+    partition's base per dtype (the view plan) and a reshape per tensor."""
+    tensors: Dict[str, object] = {}
+    parts = set(parts)
+    if scatter:
+        for t in index.tensors:
+            if t.partition in parts:
+                tensors[t.name] = per_tensor[t.name]
+        return tensors
+    tdt = _torch_dtypes()
+    for p in sorted(parts):
+        base = bases[p]
+        for dt, sizes, items in index.view_plan(p):
+            pieces = base.view(tdt[dt]).split(sizes)
+            for name, k, shape in items:
+                tensors[name] = pieces[k].view(shape)
+    return tensors
+
+
 def allocate(index: Index, gpus: Dict[int, int], scatter: bool = False, partitions: Optional[Iterable[int]] = None):
     """Destination memory through PyTorch's allocator: one uint8 base of L_p bytes per
     partition (contiguous) or one tensor per index entry (scatter)."""
@@ -547,15 +623,7 @@ def load_start(index: Index, sources: Dict[int, object], gpus: Dict[int, int], c
                                 comm.handle if comm else None, C.byref(out)))
     # The tensor objects are built while the transfer runs (the inference
     # process sets base + offset pointers before the data has arrived).
-    tensors: Dict[str, object] = {}
-    tdt = _torch_dtypes()
-    for t in index.tensors:
-        if t.partition in sources:
-            if not cfg.scatter:
-                b = bases[t.partition]
-                tensors[t.name] = b[t.offset:t.offset + t.nbytes].view(tdt[t.dtype]).view(t.shape)
-            else:
-                tensors[t.name] = per_tensor[t.name]
+    tensors = _views(index, sources.keys(), bases, per_tensor, cfg.scatter)
     return LoadResult(out, index, tensors, [dst_base, dst_tensor, st, bases, per_tensor, sources])
 
 
@@ -586,14 +654,7 @@ def load_files(index: Index, directory: str, gpus: Dict[int, int], config: Optio
     ccfg = cfg.to_c()
     check(lib().sllm_load_files_start(index.handle, C.byref(ccfg), directory.encode(), gpu, dst_base, dst_tensor, st,
                                       io_threads, comm.handle if comm else None, C.byref(out)))
-    tensors: Dict[str, object] = {}
-    tdt = _torch_dtypes()
-    for t in index.tensors:
-        if t.partition in gpus:
-            if not cfg.scatter:
-                tensors[t.name] = bases[t.partition][t.offset:t.offset + t.nbytes].view(tdt[t.dtype]).view(t.shape)
-            else:
-                tensors[t.name] = per_tensor[t.name]
+    tensors = _views(index, gpus.keys(), bases, per_tensor, cfg.scatter)
     res = LoadResult(out, index, tensors, [dst_base, dst_tensor, st, bases, per_tensor, None])
     if wait:
         res.wait()

@@ -6,6 +6,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <unordered_map>
 #include <vector>
 
@@ -61,7 +62,9 @@ struct sllm_index {
   std::string model_id;
   std::vector<sllm::PartRec> parts;
   std::vector<sllm::TensorRec> tensors;
-  std::unordered_map<std::string, uint32_t> by_name;
+  // name -> tensor id; keys view tensors[i].name (the tensor table is sized once, never
+  // reallocated after the names are entered)
+  std::unordered_map<std::string_view, uint32_t> by_name;
   uint64_t payload = 0;
   uint64_t serial = 0;  // process-unique id (device-side caches key on it)
   bool sealed = false;

@@ -110,9 +110,10 @@ static void finish_index(sllm_index* idx) {
   // per-partition tensor lists sorted by offset (used by the scatter planner)
   for (auto& p : idx->parts) p.by_offset.clear();
   for (uint32_t i = 0; i < idx->tensors.size(); ++i) idx->parts[idx->tensors[i].part].by_offset.push_back(i);
-  for (auto& p : idx->parts)
-    std::sort(p.by_offset.begin(), p.by_offset.end(),
-              [&](uint32_t a, uint32_t b) { return idx->tensors[a].offset < idx->tensors[b].offset; });
+  auto by_off = [&](uint32_t a, uint32_t b) { return idx->tensors[a].offset < idx->tensors[b].offset; };
+  for (auto& p : idx->parts)  // (source order is offset order for converter-written indexes)
+    if (!std::is_sorted(p.by_offset.begin(), p.by_offset.end(), by_off))
+      std::stable_sort(p.by_offset.begin(), p.by_offset.end(), by_off);
   idx->serial = g_serial.fetch_add(1);
 }
 
@@ -125,19 +126,21 @@ sllm_index* plan(const sllm_src_tensor* t, size_t n, uint64_t align, uint64_t bl
   idx->model_id = model_id ? model_id : "";
   std::vector<int32_t> devs;
   idx->tensors.resize(n);
+  idx->by_name.reserve(n);
   for (size_t i = 0; i < n; ++i) {
     const sllm_src_tensor& s = t[i];
     if (!s.name || !s.name[0]) fail(SLLM_E_CONVERSION, "empty tensor name");
-    std::string name(s.name);
-    if (!idx->by_name.emplace(name, (uint32_t)i).second) fail(SLLM_E_CONVERSION, "duplicate tensor name '" + name + "'");
+    TensorRec& r = idx->tensors[i];
+    r.name = s.name;
+    const std::string& name = r.name;
+    if (!idx->by_name.emplace(std::string_view(r.name), (uint32_t)i).second)
+      fail(SLLM_E_CONVERSION, "duplicate tensor name '" + name + "'");
     int w = dtype_width(s.dtype);
     if (!w) fail(SLLM_E_CONVERSION, "unknown dtype for '" + name + "'");
     if (s.device_id < 0) fail(SLLM_E_CONVERSION, "negative device id for '" + name + "'");
     if (s.ndim < 0 || s.ndim > SLLM_MAX_NDIM || (s.ndim > 0 && !s.shape))
       fail(SLLM_E_CONVERSION, "bad rank for '" + name + "'");
     unsigned __int128 numel = 1;
-    TensorRec& r = idx->tensors[i];
-    r.name = name;
     r.device = s.device_id;
     r.dtype = s.dtype;
     r.ndim = s.ndim;
@@ -397,6 +400,7 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
   // anything is sized by it
   if ((uint64_t)n_tensors * 32 > r.limit - r.pos) fail(SLLM_E_FORMAT, "tensor count exceeds the index length");
   idx->tensors.reserve(n_tensors);
+  idx->by_name.reserve(n_tensors);
   for (uint32_t i = 0; i < n_tensors; ++i) {
     TensorRec t{};
     uint32_t nl = r.get<uint32_t>();
@@ -404,7 +408,6 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
     const uint8_t* nm = r.take(nl);
     if (!valid_utf8(nm, nl)) fail(SLLM_E_FORMAT, "tensor name not UTF-8");
     t.name.assign((const char*)nm, nl);
-    if (!idx->by_name.emplace(t.name, i).second) fail(SLLM_E_FORMAT, "duplicate tensor name '" + t.name + "'");
     t.device = r.get<int32_t>();
     t.dtype = r.get<uint8_t>();
     t.ndim = r.get<uint8_t>();
@@ -431,7 +434,9 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
     if (t.offset > pr.length || t.nbytes > pr.length - t.offset) fail(SLLM_E_FORMAT, "'" + t.name + "' extends past its partition");
     count[t.part]++;
     sum += t.nbytes;
-    idx->tensors.push_back(std::move(t));
+    idx->tensors.push_back(std::move(t));  // (reserved: no reallocation, the name views stay valid)
+    const std::string& nmv = idx->tensors.back().name;
+    if (!idx->by_name.emplace(std::string_view(nmv), i).second) fail(SLLM_E_FORMAT, "duplicate tensor name '" + nmv + "'");
   }
   for (uint32_t p = 0; p < n_parts; ++p)
     if (count[p] != idx->parts[p].n_tensors) fail(SLLM_E_FORMAT, "partition tensor count mismatch");

@@ -67,6 +67,21 @@ StreamSet* DeviceCtx::acquire(int n) {
   return ss;
 }
 
+uint8_t* StreamSet::host_stage(size_t bytes) {
+  if (bytes > host_cap) {
+    if (host) cudaFreeHost(host);
+    host = nullptr;
+    host_cap = 0;
+    size_t cap = 64u << 10;
+    while (cap < bytes) cap *= 2;
+    void* h = nullptr;
+    SLLM_CUDA(cudaHostAlloc(&h, cap, cudaHostAllocPortable));
+    host = static_cast<uint8_t*>(h);
+    host_cap = cap;
+  }
+  return host;
+}
+
 void DeviceCtx::release(StreamSet* s) {
   if (s) idle.push_back(s);
 }
@@ -102,6 +117,7 @@ struct PartJob {
   uint32_t epoch = 0;
   uint32_t h_err = 0;                // peer-wait result (0 = every peer signalled)
   uint32_t* d_err = nullptr;
+  uint8_t* h_result = nullptr;  // pinned copy of {d_bad, d_err} (the set's host block)
   std::vector<Seg> segs;
   std::vector<uint32_t> chunk_seg;  // first segment of each chunk of [0, L)
   std::vector<uint32_t> gran_seg;   // scatter: last segment with off <= g MiB (MatParams.gran_seg)
@@ -342,6 +358,14 @@ static uint64_t verify_span_bytes() {
   return v;
 }
 
+// Smallest span once the end of the load is near (CE / fan-out / GDS verification): the K4
+// after the final copy covers at most this much.  kVerifyTailBytes for large partitions; an
+// eighth of the partition (>= one copy window) for small ones, so a latency-bound load
+// (e.g. an 828 MB LoRA adapter, 15 ms) does not end with a 300+ MB verification pass.
+static uint64_t verify_tail_bytes(uint64_t L) {
+  return std::min<uint64_t>(kVerifyTailBytes, std::max<uint64_t>(kWindowBytes, L / 8));
+}
+
 // Issue the window of chunks [k0, k1) of job j: the copy engine moves every chunk (one
 // batched submission), then ONE verify / scatter launch covers the window; zero-copy
 // modes issue one kernel for the window.  Returns the stream whose completion means
@@ -387,7 +411,7 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
         if (P.v_k1 == P.v_k0) P.v_k0 = k0;
         P.v_k1 = k1;
         const uint64_t pending = std::min(P.v_k1 * C, L) - P.v_k0 * C;
-        if (last || pending >= verify_span_bytes() || (pending >= kVerifyTailBytes && pending >= L - hi)) {
+        if (last || pending >= verify_span_bytes() || (pending >= verify_tail_bytes(L) && pending >= L - hi)) {
           NvtxRange nvv("sllm/verify/span [%llu,%llu)", (unsigned long long)(P.v_k0 * C),
                         (unsigned long long)std::min(P.v_k1 * C, L));
           MatParams vp = window_params(idx, cfg, j, P.v_k0, P.v_k1, P.v_k0 * C, std::min(P.v_k1 * C, L));
@@ -536,7 +560,12 @@ static void run_job(sllm_load* L, PartJob& j) {
   const size_t acc_bytes = align_up(std::max<uint64_t>(nb, 1) * sizeof(BlockAcc), 256);
   const size_t tab_bytes = align_up(std::max<uint64_t>(nb, 1) * 8, 256);
   const size_t gran_bytes = align_up(j.gran_seg.size() * 4, 256);
-  const size_t total = seg_bytes + acc_bytes + 2 * tab_bytes + 256 + gran_bytes;
+  // Device scratch: [segs | granule table | expected checksums | result word] is uploaded
+  // in ONE async copy from the set's pinned block, [block accumulators | computed
+  // checksums] is zeroed by one memset -- two setup operations ahead of the first chunk.
+  const size_t up_bytes = seg_bytes + gran_bytes + tab_bytes + 256;
+  const size_t zero_bytes = acc_bytes + tab_bytes;
+  const size_t total = up_bytes + zero_bytes;
   if (j.origin) SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[3], 0));  // recorded by sllm_load_start
   SLLM_CUDA(cudaMallocAsync(&j.scratch, total, s0));
   if (cfg.mode == SLLM_MODE_SCATTER_CE) {
@@ -544,23 +573,23 @@ static void run_job(sllm_load* L, PartJob& j) {
     SLLM_CUDA(cudaMallocAsync(&st, (size_t)P.nslot * P.slot_bytes, s0));
     j.staging = static_cast<uint8_t*>(st);
   }
+  uint8_t* h = j.ss->host_stage(up_bytes + 256);
+  j.h_result = h + up_bytes;  // 16 bytes: first failing block, peer-wait result
+  std::memcpy(h, j.segs.data(), j.segs.size() * sizeof(Seg));
+  if (!j.gran_seg.empty()) std::memcpy(h + seg_bytes, j.gran_seg.data(), j.gran_seg.size() * 4);
+  if (nb) std::memcpy(h + seg_bytes + gran_bytes, pr.checksums.data(), nb * 8);
+  std::memset(h + seg_bytes + gran_bytes + tab_bytes, 0xFF, 8);      // first failing block: none
+  std::memset(h + seg_bytes + gran_bytes + tab_bytes + 8, 0, 248);  // peer-wait result: 0
   uint8_t* base = static_cast<uint8_t*>(j.scratch);
   j.d_segs = reinterpret_cast<Seg*>(base);
-  j.d_acc = reinterpret_cast<BlockAcc*>(base + seg_bytes);
-  j.d_expect = reinterpret_cast<uint64_t*>(base + seg_bytes + acc_bytes);
-  j.d_cs = reinterpret_cast<uint64_t*>(base + seg_bytes + acc_bytes + tab_bytes);
-  j.d_bad = reinterpret_cast<unsigned long long*>(base + seg_bytes + acc_bytes + 2 * tab_bytes);
+  if (!j.gran_seg.empty()) j.d_gran_seg = reinterpret_cast<uint32_t*>(base + seg_bytes);
+  j.d_expect = reinterpret_cast<uint64_t*>(base + seg_bytes + gran_bytes);
+  j.d_bad = reinterpret_cast<unsigned long long*>(base + seg_bytes + gran_bytes + tab_bytes);
   j.d_err = reinterpret_cast<uint32_t*>(j.d_bad + 1);
-  if (!j.gran_seg.empty()) {
-    j.d_gran_seg = reinterpret_cast<uint32_t*>(base + seg_bytes + acc_bytes + 2 * tab_bytes + 256);
-    SLLM_CUDA(cudaMemcpyAsync(j.d_gran_seg, j.gran_seg.data(), j.gran_seg.size() * 4, cudaMemcpyHostToDevice, s0));
-  }
-  SLLM_CUDA(cudaMemcpyAsync(j.d_segs, j.segs.data(), j.segs.size() * sizeof(Seg), cudaMemcpyHostToDevice, s0));
-  SLLM_CUDA(cudaMemsetAsync(j.d_acc, 0, acc_bytes, s0));
-  SLLM_CUDA(cudaMemsetAsync(j.d_cs, 0, tab_bytes, s0));
-  SLLM_CUDA(cudaMemsetAsync(j.d_bad, 0xFF, 8, s0));
-  SLLM_CUDA(cudaMemsetAsync(j.d_err, 0, 8, s0));  // (the 16-byte result read covers it all)
-  if (nb) SLLM_CUDA(cudaMemcpyAsync(j.d_expect, pr.checksums.data(), nb * 8, cudaMemcpyHostToDevice, s0));
+  j.d_acc = reinterpret_cast<BlockAcc*>(base + up_bytes);
+  j.d_cs = reinterpret_cast<uint64_t*>(base + up_bytes + acc_bytes);
+  SLLM_CUDA(cudaMemcpyAsync(base, h, up_bytes, cudaMemcpyHostToDevice, s0));
+  SLLM_CUDA(cudaMemsetAsync(base + up_bytes, 0, zero_bytes, s0));
   SLLM_CUDA(cudaEventRecord(j.ev[0], s0));
   if (p2p) {  // no store into a peer replica before every peer is done verifying the previous load
     const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
@@ -619,7 +648,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       if (v.hi == v.lo) v.lo = a;
       v.hi = b;
       const uint64_t pending = v.hi - v.lo, remaining = v.end - v.hi;
-      if (remaining == 0 || pending >= verify_span_bytes() || (pending >= kVerifyTailBytes && pending >= remaining)) {
+      if (remaining == 0 || pending >= verify_span_bytes() || (pending >= verify_tail_bytes(pr.length) && pending >= remaining)) {
         verify_range(idx, cfg, j, v.lo, v.hi, cs);
         v.lo = v.hi = 0;
       }
@@ -706,7 +735,7 @@ static void run_job(sllm_load* L, PartJob& j) {
                  if (v_hi == v_lo) v_lo = a;
                  v_hi = b;
                  const uint64_t pending = v_hi - v_lo, remaining = pr.length - v_hi;
-                 if (remaining == 0 || pending >= verify_span_bytes() || (pending >= kVerifyTailBytes && pending >= remaining)) {
+                 if (remaining == 0 || pending >= verify_span_bytes() || (pending >= verify_tail_bytes(pr.length) && pending >= remaining)) {
                    verify_range(idx, cfg, j, v_lo, v_hi, P.kern);
                    v_lo = v_hi = 0;
                  }
@@ -722,13 +751,15 @@ static void run_job(sllm_load* L, PartJob& j) {
   // join every stream into s0, then let the caller's stream wait for the load
   join_streams(tails, s0);
   SLLM_CUDA(cudaEventRecord(j.ev[1], s0));
+  // the result word comes back into the pinned block behind the load (no extra round trip)
+  SLLM_CUDA(cudaMemcpyAsync(j.h_result, j.d_bad, 16, cudaMemcpyDeviceToHost, s0));
   {  // every command of this job is enqueued: the caller's stream may now wait on ev[1]
     std::lock_guard<std::mutex> g(L->issue_mu);
     j.issue_ok = j.issue_signalled = true;
   }
   L->issue_cv.notify_all();
   j.t_issue_ns = now_ns() - t0;
-  SLLM_CUDA(cudaEventSynchronize(j.ev[1]));
+  SLLM_CUDA(cudaStreamSynchronize(s0));  // the load (ev[1]) and its result word
   if (j.staging) {
     // The SCATTER_CE staging ring is not part of the loaded model: back to the stream-ordered
     // pool as soon as the load is done (reusable by the next load at no cost; re-growing a
@@ -743,7 +774,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   }
   j.fsrc.reset();  // file tier: readers are done, slots go back to the pinned pool
   uint64_t tail[2] = {};
-  SLLM_CUDA(cudaMemcpy(tail, j.d_bad, 16, cudaMemcpyDeviceToHost));  // first failing block, peer-wait result
+  std::memcpy(tail, j.h_result, 16);  // first failing block, peer-wait result
   j.h_bad = tail[0];
   j.h_err = (uint32_t)tail[1];
   SLLM_CUDA(cudaEventElapsedTime(&j.t_dev_ms, j.ev[0], j.ev[1]));
@@ -755,11 +786,14 @@ static void run_job(sllm_load* L, PartJob& j) {
       float ms = 0;
       SLLM_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
       sum += ms;
-      if (dump && v == &j.kev) {
+      if (dump) {
         float at = 0;
         SLLM_CUDA(cudaEventElapsedTime(&at, j.ev[0], e.first));
-        fprintf(stderr, "sllm-prof p=%zu kernel=%zu start_ms=%.4f ms=%.4f bytes=%llu GBps=%.1f\n", j.p, i, at, ms,
-                (unsigned long long)j.kev_bytes[i], j.kev_bytes[i] / (ms * 1e6));
+        if (v == &j.kev)
+          fprintf(stderr, "sllm-prof p=%zu kernel=%zu start_ms=%.4f ms=%.4f bytes=%llu GBps=%.1f\n", j.p, i, at, ms,
+                  (unsigned long long)j.kev_bytes[i], j.kev_bytes[i] / (ms * 1e6));
+        else
+          fprintf(stderr, "sllm-prof p=%zu copy=%zu start_ms=%.4f ms=%.4f\n", j.p, i, at, ms);
       }
       cudaEventDestroy(e.first);
       cudaEventDestroy(e.second);

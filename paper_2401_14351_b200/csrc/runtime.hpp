@@ -60,6 +60,11 @@ struct StreamSet {
   cudaStream_t xfer[kMaxStreams] = {};
   cudaStream_t kern = nullptr;
   cudaStream_t comm = nullptr;
+  // pinned host block of the job holding the set: its per-load tables go up in ONE async
+  // copy and its result word comes back into it (grown on demand, kept for the next job)
+  uint8_t* host = nullptr;
+  size_t host_cap = 0;
+  uint8_t* host_stage(size_t bytes);  // caller holds the set (exclusive), device set
 };
 struct DeviceCtx {
   int dev = -1;

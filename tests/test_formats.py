@@ -160,3 +160,42 @@ def test_state_dict_front_end(tmp_path):
     with pytest.raises(_abi.SllmError) as ex:                  # unsupported dtype
         formats.convert_state_dict({"x": np.zeros(3, np.complex64)}, str(tmp_path / "bad"))
     assert ex.value.status == _abi.E_CONVERSION
+
+
+def test_view_plan_matches_base_plus_offset():
+    """The grouped-split views of a contiguous load are exactly base[off:off+size] as
+    dtype/shape (P:549 base + offset), for random inventories with all twelve dtypes,
+    scalars and padding -- checked on a CPU tensor standing in for the device base."""
+    import numpy as np
+    import torch
+    import paper_2401_14351_b200 as sllm
+    from paper_2401_14351_b200 import api
+    from synth import models
+    for seed in range(6):
+        rng = np.random.default_rng(500 + seed)
+        inv = models.random_inventory(rng, 150, 3, 1 << 20)
+        idx = sllm.Index.plan([(t.name, t.device, t.dtype, t.shape) for t in inv], int(rng.choice([16, 4096])), 0)
+        bases = {p: torch.from_numpy(rng.integers(0, 256, q.length, dtype=np.uint8))
+                 for p, q in enumerate(idx.partitions)}
+        views = api._views(idx, bases.keys(), bases, None, False)
+        assert len(views) == len(inv)
+        for t in idx.tensors:
+            v = views[t.name]
+            assert tuple(v.shape) == t.shape and v.dtype == api._torch_dtypes()[t.dtype]
+            assert v.data_ptr() == bases[t.partition].data_ptr() + t.offset
+            raw = v.reshape(-1).view(torch.uint8) if v.dim() else v.reshape(1).view(torch.uint8)
+            assert torch.equal(raw, bases[t.partition][t.offset:t.offset + t.nbytes])
+
+
+def test_derived_tables_shared_by_content():
+    """Index objects parsed from the same bytes share their Python tensor table (a1 still
+    parses and validates every time); different content gets its own."""
+    import paper_2401_14351_b200 as sllm
+    from synth import models
+    inv = models.toy()
+    blob = sllm.Index.plan([(t.name, t.device, t.dtype, t.shape) for t in inv], 4096, 0).serialize()
+    a, b = sllm.Index.from_bytes(blob), sllm.Index.from_bytes(blob)
+    assert a.tensors is b.tensors and a.handle.value != b.handle.value
+    other = sllm.Index.from_bytes(sllm.Index.plan([(t.name, t.device, t.dtype, t.shape) for t in inv[:-1]],
+                                                  4096, 0).serialize())
+    assert other.tensors is not a.tensors and len(other.tensors) == len(inv) - 1

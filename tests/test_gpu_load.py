@@ -371,3 +371,30 @@ def test_auto_mode_picks_by_size():
         t = big[e]
         got = res2.tensors[t.name].reshape(-1).view(torch.uint8)[:4096].cpu().numpy()
         assert np.array_equal(got, payload.payload_bytes(9, e, t.nbytes)[:4096])
+
+
+@pytest.mark.parametrize("mode", MODES + ["auto"])
+def test_lora_adapter_all_modes_bit_exact(mode):
+    """the rank-32 LoRA adapter of LLaMA-2-70B (828 MB, 1,120 small
+    tensors -- the paper's ~1 GB adapter) in every mode: every tensor byte-equal
+    to its payload, every block checksum equal to the oracle's table, the whole partition
+    (padding included) equal to the oracle's bytes in the contiguous modes."""
+    inv, seed = models.model_inventory("lora-70b-r32")
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    lay, oparts, payloads = _lora_oracle()
+    cfg = sllm.LoadConfig(chunk_bytes=16 << 20, mode=mode)
+    res = sllm.load(idx, bufs, {0: 0}, cfg)
+    assert len(res.tensors) == 1120
+    check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
+    if mode == "auto":   # < 256 MiB per job picks zero-copy; 828 MB stays on the copy engine
+        assert res.report["mode"] == 0
+
+
+_LORA = {}
+
+
+def _lora_oracle():
+    if not _LORA:
+        inv, seed = models.model_inventory("lora-70b-r32")
+        _LORA["v"] = oracle_of(inv, seed, 4096, 1 << 20)
+    return _LORA["v"]
