@@ -9,7 +9,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsllm.so")
+# SLLM_LIB_PATH: an A/B measurement build of the same sources (tools/build_variant.py);
+# the product path is the in-tree libsllm.so
+LIB_PATH = os.environ.get("SLLM_LIB_PATH") or os.path.join(HERE, "libsllm.so")
 
 MAX_NDIM = 8
 

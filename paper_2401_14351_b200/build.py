@@ -59,19 +59,25 @@ def _headers():
 SAN_FLAGS = "-fsanitize=address,-fsanitize=undefined,-fno-omit-frame-pointer,-fno-sanitize-recover=all"
 
 
-def build(force: bool = False, verbose: bool = False, sanitize: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, sanitize: bool = False, variant: str = "",
+          defines=()) -> str:
     """sanitize=True: an AddressSanitizer + UBSan build of the host code (kernels unchanged)
-    at build/sllm_asan/libsllm_asan.so, for tests/test_sanitizers.py -- never the product."""
+    at build/sllm_asan/libsllm_asan.so, for tests/test_sanitizers.py -- never the product.
+    variant="name", defines=[...]: an A/B measurement build at build/ab/<name>/libsllm.so
+    (loaded with SLLM_LIB_PATH) -- never the product."""
     srcs = sources()
     out = os.path.join(ROOT, "build", "sllm_asan", "libsllm_asan.so") if sanitize else OUT
     bdir = os.path.join(ROOT, "build", "sllm_asan") if sanitize else BUILD
+    if variant:
+        bdir = os.path.join(ROOT, "build", "ab", variant)
+        out = os.path.join(bdir, "libsllm.so")
     newest = max(os.path.getmtime(p) for p in srcs + _headers() + [__file__])
     if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
         return out
     os.makedirs(bdir, exist_ok=True)
     nvcc = _nvcc()
     host = "-fPIC,-O3,-fvisibility=hidden" if not sanitize else "-fPIC,-O1,-g,-fvisibility=hidden," + SAN_FLAGS
-    extra = os.environ.get("SLLM_NVCC_DEFINES", "").split()  # A/B builds only, e.g. "-DSLLM_STAGE_KIB=32"
+    extra = os.environ.get("SLLM_NVCC_DEFINES", "").split() + list(defines)  # A/B builds only, e.g. "-DSLLM_STAGE_KIB=32"
     common = ["-O3", "-std=c++17", "-lineinfo", *ARCH, *extra, "-Xcompiler", host,
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()]
 

@@ -197,6 +197,12 @@ constexpr int kStoreLag = 4;                             // bulk-store groups in
 #define SLLM_STAGE_KIB 16
 #endif
 constexpr int kConsumerUnroll = SLLM_CONSUMER_UNROLL;
+// Lanes of the producer warp issuing bulk copies (A/B knob: "several producer
+// lanes" for the zero-copy host reads; profiles/r02/zc_ab.jsonl)
+#ifndef SLLM_PRODUCER_LANES
+#define SLLM_PRODUCER_LANES 1
+#endif
+constexpr int kProducerLanes = SLLM_PRODUCER_LANES;
 constexpr uint32_t kStageBytes = SLLM_STAGE_KIB << 10;  // ring: kStages x kStageBytes = 192 KiB
 constexpr int kStages = (192 << 10) / kStageBytes;
 constexpr uint64_t kMaxUnitBytes = 1ull << 20;  // default: whole 1 MiB blocks when the launch is balanced
@@ -299,12 +305,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   }
   __syncthreads();
 
-  if (warp == 0) {  // producer
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
+  if (warp == 0) {  // producer (kProducerLanes lanes issue the stages round-robin; default 1)
+    if (lane < kProducerLanes) {
+      uint32_t stage = 0, phase = 0, seq = 0;
       for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x) {
         const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
-        for (uint64_t off = a; off < e; off += kStageBytes) {
+        for (uint64_t off = a; off < e; off += kStageBytes, ++seq) {
+          if (kProducerLanes > 1 && seq % kProducerLanes != (uint32_t)lane) {
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+            continue;
+          }
           const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
           mbar_wait(&empty[stage], phase ^ 1);
           // the consumers' generic-proxy reads of this stage (ordered before their empty
