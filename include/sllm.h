@@ -282,8 +282,12 @@ typedef enum {
  *           Here rank r's PCIe share is not a contiguous slice but every chunk k with
  *           k mod nranks == r (sllm_allgather_round), so the whole partition must be pinned;
  *           pinned sources only (not sllm_load_files_start).
+ *   NVLS  : as P2P, but every vector is stored ONCE through an NVLink-
+ *           SHARP multicast address (multimem.st) and the NVSwitch writes it into every
+ *           replica of the group; the group and its replicas come from sllm_comm_init_nvls.
  * Every rank's received bytes are verified against the index like its own (K4). */
-typedef enum { SLLM_FANOUT_NONE = 0, SLLM_FANOUT_BCAST = 1, SLLM_FANOUT_P2P = 2, SLLM_FANOUT_ALLGATHER = 3 } sllm_fanout;
+typedef enum { SLLM_FANOUT_NONE = 0, SLLM_FANOUT_BCAST = 1, SLLM_FANOUT_P2P = 2, SLLM_FANOUT_ALLGATHER = 3,
+               SLLM_FANOUT_NVLS = 4 } sllm_fanout;
 
 typedef struct {
   uint64_t chunk_bytes; /* multiple of the index block size (and of align); 0 = 16 MiB    */
@@ -349,6 +353,22 @@ SLLM_API sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_com
  * The handle owns its streams; sllm_comm_free releases them (never the replicas). */
 SLLM_API sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
                                           uint32_t* const* peer_signal, uint64_t timeout_ms, sllm_comm** out);
+/* NVLS multicast group for SLLM_FANOUT_NVLS (the fan-out fused into the
+ * loading kernel, replicated by the NVSwitch).  One process drives every GPU of the group
+ * (P:721-727): handle i is rank i on gpus[i] (n = 1..8, distinct).  The library creates one
+ * multicast object (cuMulticastCreate), allocates and binds a replica of >= `bytes` on every
+ * GPU (cuMemCreate; the replica is LIBRARY-owned, freed with the last handle of the group:
+ * sllm_comm_replica gives its address) and maps the multicast address.  Loads of the group
+ * pass dst_base[0] = that replica.  timeout_ms as in sllm_comm_init_peers (0 = 60000).
+ * Capability-gated: SLLM_E_INVALID (message names the failing driver call) when a GPU lacks
+ * multicast support or the platform cannot create the object (no NVSwitch / NVLS fabric) --
+ * keep the P2P or NCCL fan-out then.  SLLM_E_CAPACITY when a replica cannot be allocated. */
+SLLM_API sllm_status sllm_comm_init_nvls(const int32_t* gpus, int32_t n, uint64_t bytes, uint64_t timeout_ms,
+                                         sllm_comm** out /* n handles */);
+/* The replica a P2P / NVLS group handle is bound to: *base = this rank's replica (device
+ * pointer), *bytes (may be NULL) = its size for an NVLS group (library-owned), 0 for a P2P
+ * group (caller-owned).  SLLM_E_INVALID for an NCCL communicator. */
+SLLM_API sllm_status sllm_comm_replica(const sllm_comm* comm, void** base, uint64_t* bytes);
 SLLM_API void sllm_comm_free(sllm_comm* comm);
 
 /* Start loading (asynchronous: returns once worker threads are launched).

@@ -21,7 +21,7 @@ STATUS = {0: "OK", 1: "INVALID", 2: "CONVERSION", 3: "FORMAT", 4: "LOOKUP", 5: "
  E_PEER) = range(13)
 
 MODE_CE, MODE_ZEROCOPY, MODE_SCATTER_CE, MODE_SCATTER_ZC, MODE_AUTO, MODE_GDS = range(6)
-FANOUT_NONE, FANOUT_BCAST, FANOUT_P2P, FANOUT_ALLGATHER = range(4)
+FANOUT_NONE, FANOUT_BCAST, FANOUT_P2P, FANOUT_ALLGATHER, FANOUT_NVLS = range(5)
 DTYPE_CODE = {"f16": 0, "bf16": 1, "f32": 2, "i8": 3, "u8": 4, "i64": 5,
               "i32": 6, "f64": 7, "i16": 8, "bool": 9, "f8e4m3": 10, "f8e5m2": 11}
 DTYPE_NAME = {v: k for k, v in DTYPE_CODE.items()}
@@ -117,6 +117,8 @@ SIGNATURES = {
     "sllm_comm_init_rank": (S, [P, C.c_int32, C.c_int32, C.c_int32, PP]),
     "sllm_comm_init_all": (S, [C.POINTER(C.c_int32), C.c_int32, PP]),
     "sllm_comm_init_peers": (S, [C.c_int32, C.c_int32, C.c_int32, PP, PP, U64, PP]),
+    "sllm_comm_init_nvls": (S, [C.POINTER(C.c_int32), C.c_int32, U64, U64, PP]),
+    "sllm_comm_replica": (S, [P, PP, C.POINTER(U64)]),
     "sllm_comm_free": (None, [P]),
     "sllm_cache_create": (S, [U64, C.c_int32, C.c_int32, PP]),
     "sllm_cache_acquire": (S, [P, C.c_char_p, C.c_int32, PP, C.POINTER(PP), C.POINTER(C.c_int32)]),

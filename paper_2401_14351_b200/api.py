@@ -279,7 +279,8 @@ def fanout_unit(chunk: int, fanout: str) -> int:
     """sllm_fanout_unit: the slice / round unit a load with this chunk size and fan-out uses
     (NCCL fan-outs: a whole >= 64 MiB window of chunks)."""
     out = C.c_uint64()
-    check(lib().sllm_fanout_unit(chunk, {"none": 0, "bcast": 1, "p2p": 2, "allgather": 3}[fanout], C.byref(out)))
+    check(lib().sllm_fanout_unit(chunk, {"none": 0, "bcast": 1, "p2p": 2, "allgather": 3, "nvls": 4}[fanout],
+                                 C.byref(out)))
     return out.value
 
 
@@ -391,7 +392,7 @@ class LoadConfig:
     chunk_bytes: int = 16 << 20   # P:1279 "16MB" (read as MiB, Q9)
     n_streams: int = 2
     mode: str = "ce"              # ce | zerocopy | scatter_ce | scatter_zc | auto (ce or zerocopy by size) | gds (files)
-    fanout: str = "none"          # none | bcast / allgather (NCCL) | p2p (fused NVLink stores)
+    fanout: str = "none"          # none | bcast / allgather (NCCL) | p2p (fused NVLink stores) | nvls (multicast)
     verify: bool = True
     ctas: int = 0
     profile: bool = False         # per-launch CUDA-event timing (bench roofline)
@@ -401,7 +402,7 @@ class LoadConfig:
         modes = {"ce": _abi.MODE_CE, "zerocopy": _abi.MODE_ZEROCOPY, "scatter_ce": _abi.MODE_SCATTER_CE,
                  "scatter_zc": _abi.MODE_SCATTER_ZC, "auto": _abi.MODE_AUTO, "gds": _abi.MODE_GDS}
         fan = {"none": _abi.FANOUT_NONE, "bcast": _abi.FANOUT_BCAST, "p2p": _abi.FANOUT_P2P,
-               "allgather": _abi.FANOUT_ALLGATHER}
+               "allgather": _abi.FANOUT_ALLGATHER, "nvls": _abi.FANOUT_NVLS}
         return _abi.LoadConfig(self.chunk_bytes, self.n_streams, modes[self.mode], fan[self.fanout],
                                int(self.verify), self.ctas, int(self.profile),
                                {"tma": 1, "ldg": 2, "tma_store": 3}[self.engine], 0)
@@ -489,6 +490,35 @@ class Comm:
         c = cls.peers(world, rank, gpu, bases, sigs, timeout_ms, keep=[base, sig])
         c._opened = opened
         return c
+
+    @classmethod
+    def nvls(cls, gpus: Sequence[int], nbytes: int, timeout_ms: int = 0) -> List["Comm"]:
+        """sllm_comm_init_nvls: an NVLink-SHARP multicast group over ``gpus`` driven by this
+        process (handle i = rank i on gpus[i]) with library-owned replicas of >= ``nbytes``
+        bound to it.  Raises SllmError(SLLM_E_INVALID) where the platform cannot create
+        multicast objects (no NVSwitch fabric)."""
+        n = len(gpus)
+        arr = (C.c_int32 * n)(*[int(g) for g in gpus])
+        out = (C.c_void_p * n)()
+        check(lib().sllm_comm_init_nvls(arr, n, int(nbytes), int(timeout_ms), out))
+        comms = [cls(out[i]) for i in range(n)]
+        for i, c in enumerate(comms):
+            c._gpu = int(gpus[i])
+            c._group = comms          # the replicas live while any handle of the group does
+        return comms
+
+    def replica(self):
+        """The replica a P2P / NVLS handle is bound to, as a zero-copy torch uint8 tensor
+        (NVLS: library-owned memory, valid while the group's handles live)."""
+        import torch
+        base, n = C.c_void_p(), C.c_uint64()
+        check(lib().sllm_comm_replica(self._h, C.byref(base), C.byref(n)))
+
+        class _Mem:  # __cuda_array_interface__ view of the library's allocation
+            __cuda_array_interface__ = {"shape": (n.value,), "typestr": "|u1", "data": (base.value, False),
+                                        "version": 3, "strides": None}
+        t = torch.as_tensor(_Mem(), device=f"cuda:{getattr(self, '_gpu', 0)}")
+        return t
 
     @property
     def handle(self):

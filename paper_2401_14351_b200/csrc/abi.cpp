@@ -37,6 +37,8 @@ sllm_comm* sllm_comm_init_rank_internal(const void*, int32_t, int32_t, int32_t);
 void sllm_comm_init_all_internal(const int32_t*, int32_t, sllm_comm**);
 sllm_comm* sllm_comm_init_peers_internal(int32_t, int32_t, int32_t, void* const*, uint32_t* const*, uint64_t);
 void sllm_comm_free_internal(sllm_comm*);
+void sllm_comm_init_nvls_internal(const int32_t*, int32_t, uint64_t, uint64_t, sllm_comm**);
+void sllm_comm_replica_internal(const sllm_comm*, void**, uint64_t*);
 namespace sllm {
 sllm_cache* cache_create(uint64_t capacity, int gpu, int pin);
 void cache_acquire(sllm_cache* c, const char* dir, int io_threads, const sllm_index** index, void* const** bufs,
@@ -364,6 +366,14 @@ sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void
     if (!out) fail(SLLM_E_INVALID, "null out");
     *out = sllm_comm_init_peers_internal(nranks, rank, gpu, peer_base, peer_signal, timeout_ms);
   });
+}
+
+sllm_status sllm_comm_init_nvls(const int32_t* gpus, int32_t n, uint64_t bytes, uint64_t timeout_ms, sllm_comm** out) {
+  return guard_dev([&] { sllm_comm_init_nvls_internal(gpus, n, bytes, timeout_ms, out); });
+}
+
+sllm_status sllm_comm_replica(const sllm_comm* c, void** base, uint64_t* bytes) {
+  return guard([&] { sllm_comm_replica_internal(c, base, bytes); });
 }
 
 void sllm_comm_free(sllm_comm* c) {

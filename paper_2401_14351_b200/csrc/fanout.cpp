@@ -100,6 +100,10 @@ struct sllm_comm {
   uint64_t timeout_ns = 0;
   cudaStream_t streams[sllm::kMaxStreams + 1] = {};
   std::shared_ptr<sllm::LocalGroup> local;  // the in-process ranks of this peer group
+  // NVLS group (SLLM_FANOUT_NVLS): the multicast object and the library-owned replicas it
+  // binds (shared by the group's handles); mc = the multicast address of replica byte 0
+  std::shared_ptr<sllm::NvlsGroup> nvls;
+  uint8_t* mc = nullptr;
 };
 
 namespace sllm {
@@ -115,6 +119,7 @@ int comm_device(const sllm_comm* c) { return c->dev; }
 bool comm_is_peers(const sllm_comm* c) { return c->peers; }
 uint8_t* comm_peer_base(const sllm_comm* c, int q) { return c->base[q]; }
 uint32_t* comm_peer_signal(const sllm_comm* c, int q) { return c->signal[q]; }
+uint8_t* comm_mc(const sllm_comm* c) { return c->mc; }
 uint64_t comm_timeout_ns(const sllm_comm* c) { return c->timeout_ns; }
 uint32_t comm_next_epoch(sllm_comm* c) {
   if (++c->epoch == 0) ++c->epoch;  // 0 is the signal arrays' initial value
@@ -251,10 +256,49 @@ sllm_comm* sllm_comm_init_peers_internal(int32_t nranks, int32_t rank, int32_t g
   return c.release();
 }
 
+// NVLS group: one process, GPUs gpus[0..n-1]; handle i is rank i on
+// gpus[i].  The fan-out runs the P2P group's protocol (slices, ready/done epochs, received
+// ranges verified by K4) with every vector stored once through the multicast address.
+void sllm_comm_init_nvls_internal(const int32_t* gpus, int32_t n, uint64_t bytes, uint64_t timeout_ms,
+                                  sllm_comm** out) {
+  if (!out) fail(SLLM_E_INVALID, "null out");
+  std::shared_ptr<NvlsGroup> g = nvls_group_create(gpus, n, bytes);
+  auto local = std::make_shared<LocalGroup>();
+  local->members = n;
+  std::vector<std::unique_ptr<sllm_comm>> cs;
+  for (int i = 0; i < n; ++i) {
+    std::unique_ptr<sllm_comm> c(new sllm_comm);
+    c->nranks = n;
+    c->rank = i;
+    c->dev = gpus[i];
+    c->peers = true;
+    c->timeout_ns = (timeout_ms ? timeout_ms : 60000ull) * 1000000ull;
+    for (int q = 0; q < n; ++q) {
+      c->base.push_back(nvls_replica(*g, q));
+      c->signal.push_back(nvls_signal(*g, q));
+    }
+    c->nvls = g;
+    c->mc = nvls_mc(*g);
+    if (n > 1) c->local = local;
+    cs.push_back(std::move(c));
+  }
+  for (int i = 0; i < n; ++i) out[i] = cs[i].release();
+}
+
+void sllm_comm_replica_internal(const sllm_comm* c, void** base, uint64_t* bytes) {
+  if (!c || !base) fail(SLLM_E_INVALID, "null argument");
+  if (!c->peers) fail(SLLM_E_INVALID, "an NCCL communicator is not bound to a replica");
+  *base = c->base[c->rank];
+  if (bytes) *bytes = c->nvls ? nvls_size(*c->nvls) : 0;
+}
+
 void sllm_comm_free_internal(sllm_comm* c) {
   if (!c) return;
   if (c->comm && g_nccl_ok) g_nccl.CommDestroy(c->comm);
-  if (c->local) {
+  if (c->local && c->nvls) {  // (an NVLS group's local share is not in the registry)
+    std::lock_guard<std::mutex> lg(c->local->mu);
+    --c->local->members;
+  } else if (c->local) {
     std::lock_guard<std::mutex> g(g_groups_mu);
     {
       std::lock_guard<std::mutex> lg(c->local->mu);

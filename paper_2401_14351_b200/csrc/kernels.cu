@@ -47,6 +47,13 @@ __device__ __forceinline__ uint4 load16(const uint8_t* p) {
   return r;
 }
 
+// NVLS: one store through the multicast address reaches every replica bound to it (the
+// 32-bit lanes are moved, never converted: an .f32 store is a bit copy)
+__device__ __forceinline__ void mc_store16(uint8_t* p, const uint4& v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
 __device__ __forceinline__ void store16(uint8_t* p, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   // engine 2: the tensor bytes leave shared memory by TMA bulk stores issued by one
   // storer thread (contiguous pieces: segment x stage); consumers then only read smem for
   // the checksum and write the < 16-byte tails of tensors.
-  const bool bulk_store = kStore && p.engine == 2 && p.n_peers == 0 && !p.no_seg_store;
+  const bool bulk_store = kStore && p.engine == 2 && p.n_peers == 0 && !p.mc && !p.no_seg_store;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
@@ -389,7 +396,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
       for (uint32_t v = (uint32_t)ct * 16; v < n; v += 32 * kConsumerWarps * 16) {
         const uint4 val = lds16(sb + v);
         const uint64_t x = off + v;
-        if (kStore) {
+        if (kStore && p.mc) {
+          mc_store16(p.mc + x, val);  // NVLS fan-out (contiguous): every replica at once
+        } else if (kStore) {
           while (x >= sg.off + sg.len && cur + 1 < p.seg_end) sg = p.segs[++cur];
           if (sg.dst && !p.no_seg_store) {
             const uint64_t rel = x - sg.off;

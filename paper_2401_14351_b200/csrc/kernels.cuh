@@ -56,6 +56,9 @@ struct MatParams {
   uint32_t n_peers;
   uint32_t no_seg_store;
   uint8_t* peer[kMaxPeers];
+  // NVLS fan-out: multicast address of partition byte 0 -- every vector is stored once with
+  // multimem.st and lands in every replica of the group (own included); no per-segment store
+  uint8_t* mc;
 };
 
 enum class MatKind : int {

@@ -114,6 +114,7 @@ struct PartJob {
   // P2P fan-out: the peers' replicas (device pointers valid here), this load's epoch
   uint8_t* peers[kMaxPeers] = {};
   uint32_t n_peers = 0;
+  uint8_t* mc = nullptr;             // NVLS fan-out: multicast address of replica byte 0
   uint32_t epoch = 0;
   uint32_t h_err = 0;                // peer-wait result (0 = every peer signalled)
   uint32_t* d_err = nullptr;
@@ -300,6 +301,7 @@ static MatParams window_params(const sllm_index& idx, const sllm_load_config& cf
   mp.engine = kernel_engine(cfg.engine);
   mp.n_peers = j.n_peers;
   for (uint32_t k = 0; k < j.n_peers; ++k) mp.peer[k] = j.peers[k];
+  mp.mc = j.mc;
   return mp;
 }
 
@@ -389,9 +391,10 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
   switch (cfg.mode) {
     case SLLM_MODE_CE:
       copy_window(j, prof, j.dst_base + lo, wsrc, lo, k0, k1, C, L, xs);
-      if (j.n_peers) {
-        // P2P fan-out: one kernel per landed window reads it back from the rank's own
-        // replica, verifies it and stores it into every peer replica over NVLink
+      if (j.n_peers || j.mc) {
+        // P2P / NVLS fan-out: one kernel per landed window reads it back from the rank's own
+        // replica, verifies it and stores it into every peer replica over NVLink (NVLS: one
+        // multicast store per vector)
         SLLM_CUDA(cudaEventRecord(P.copied, xs));
         SLLM_CUDA(cudaStreamWaitEvent(P.kern, P.copied, 0));
         mp.src = j.dst_base;
@@ -503,7 +506,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   }
   Pipe P;
   P.S = cfg.n_streams;
-  const bool p2p = cfg.fanout == SLLM_FANOUT_P2P;
+  const bool p2p = cfg.fanout == SLLM_FANOUT_P2P || cfg.fanout == SLLM_FANOUT_NVLS;  // (same group protocol)
   for (int s = 0; s < P.S; ++s) P.xfer[s] = p2p ? comm_stream(L->comm, s) : j.ss->xfer[s];
   P.kern = p2p ? comm_stream(L->comm, kMaxStreams) : j.ss->kern;
   P.nslot = std::max(3, P.S + 1);
@@ -875,10 +878,16 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   if (idx->block && cfg.chunk_bytes % idx->block) fail(SLLM_E_INVALID, "chunk size must be a multiple of the block size");
   if (cfg.chunk_bytes % idx->align) fail(SLLM_E_INVALID, "chunk size must be a multiple of the alignment");
   const bool scatter = cfg.mode == SLLM_MODE_SCATTER_CE || cfg.mode == SLLM_MODE_SCATTER_ZC;
-  if (cfg.fanout == SLLM_FANOUT_BCAST || cfg.fanout == SLLM_FANOUT_P2P || cfg.fanout == SLLM_FANOUT_ALLGATHER) {
+  const bool group_fanout = cfg.fanout == SLLM_FANOUT_P2P || cfg.fanout == SLLM_FANOUT_NVLS;
+  if (cfg.fanout == SLLM_FANOUT_BCAST || group_fanout || cfg.fanout == SLLM_FANOUT_ALLGATHER) {
     if (!comm) fail(SLLM_E_INVALID, "fan-out needs a communicator");
-    if (cfg.fanout != SLLM_FANOUT_P2P && comm_is_peers(comm))
+    if (!group_fanout && comm_is_peers(comm))
       fail(SLLM_E_INVALID, "SLLM_FANOUT_BCAST/ALLGATHER need an NCCL communicator (sllm_comm_init_rank/_all)");
+    if (cfg.fanout == SLLM_FANOUT_NVLS && !comm_mc(comm))
+      fail(SLLM_E_INVALID, "SLLM_FANOUT_NVLS needs an NVLS group (sllm_comm_init_nvls)");
+    if (cfg.fanout == SLLM_FANOUT_P2P && comm_mc(comm))
+      fail(SLLM_E_INVALID, "an NVLS group's replicas take multicast stores only: use SLLM_FANOUT_NVLS");
+    if (cfg.fanout == SLLM_FANOUT_NVLS && cfg.engine == 2) fail(SLLM_E_INVALID, "the NVLS fan-out needs the TMA engine");
     if (cfg.fanout == SLLM_FANOUT_ALLGATHER && dir)
       fail(SLLM_E_INVALID, "SLLM_FANOUT_ALLGATHER loads from pinned sources only (its chunks are strided)");
     if (cfg.fanout == SLLM_FANOUT_P2P && !comm_is_peers(comm))
@@ -929,11 +938,15 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
         j.hi = idx->parts[p].length;
       }
     }
-    if (cfg.fanout == SLLM_FANOUT_P2P) {
+    if (group_fanout) {
       if (j.dst_base != comm_peer_base(comm, comm_rank(comm)))
-        fail(SLLM_E_INVALID, "P2P fan-out: dst_base must be this rank's replica of the peer group");
-      for (int q = 0; q < comm_nranks(comm); ++q)
-        if (q != comm_rank(comm)) j.peers[j.n_peers++] = comm_peer_base(comm, q);
+        fail(SLLM_E_INVALID, "P2P / NVLS fan-out: dst_base must be this rank's replica of the group");
+      if (cfg.fanout == SLLM_FANOUT_NVLS) {
+        j.mc = comm_mc(comm);
+      } else {
+        for (int q = 0; q < comm_nranks(comm); ++q)
+          if (q != comm_rank(comm)) j.peers[j.n_peers++] = comm_peer_base(comm, q);
+      }
     }
     if (j.dst_base && (reinterpret_cast<uintptr_t>(j.dst_base) & 15)) fail(SLLM_E_INVALID, "dst_base must be 16-byte aligned");
     if (scatter) {
@@ -995,7 +1008,7 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
       for (auto& e : j.ev) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
       if (j.origin) {
         SLLM_CUDA(cudaEventRecord(j.ev[3], j.origin));
-        j.eager = j.file.empty() && !(cfg.fanout == SLLM_FANOUT_P2P && comm_local_members(comm) > 1);
+        j.eager = j.file.empty() && !(group_fanout && comm_local_members(comm) > 1);
       }
     }
   } catch (...) {
@@ -1007,7 +1020,7 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
     }
     throw;
   }
-  if (cfg.fanout == SLLM_FANOUT_P2P)  // one epoch per collective load, taken in call order
+  if (group_fanout)  // one epoch per collective load, taken in call order
     for (auto& j : L->jobs) j.epoch = comm_next_epoch(comm);
   for (auto& j : L->jobs) j.th = std::thread(run_job_guarded, L.get(), std::ref(j));
   // Caller-stream ordering without a device-side gate: a stream waiting for work that is not

@@ -108,6 +108,15 @@ uint8_t* comm_peer_base(const sllm_comm* c, int q);
 uint32_t* comm_peer_signal(const sllm_comm* c, int q);
 uint64_t comm_timeout_ns(const sllm_comm* c);
 uint32_t comm_next_epoch(sllm_comm* c);
+uint8_t* comm_mc(const sllm_comm* c);  // NVLS: multicast address of replica byte 0 (else null)
+
+// ---- NVLS multicast group (nvls.cpp) -------------------------------------------------
+struct NvlsGroup;
+std::shared_ptr<NvlsGroup> nvls_group_create(const int32_t* gpus, int32_t n, uint64_t bytes);
+size_t nvls_size(const NvlsGroup& g);
+uint8_t* nvls_mc(const NvlsGroup& g);
+uint8_t* nvls_replica(const NvlsGroup& g, int i);
+uint32_t* nvls_signal(const NvlsGroup& g, int i);
 void comm_local_barrier(sllm_comm* c);
 
 // GPUDirect Storage reads (gds.cpp): file bytes [lo, hi) -> dst + lo on `gpu`, `threads`

@@ -248,3 +248,75 @@ def test_fanout_one_process_per_gpu(kind, mode):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok, _ in out), out
+
+
+# ---- NVLS multicast fan-out ---------------------------------------
+def _nvls_or_skip(gpus, nbytes):
+    """The group, or a skip naming why the platform cannot create multicast objects (the
+    library's clean SLLM_E_INVALID; this build's 1-GPU VMs, profiles/r01/probe_nvls.txt)."""
+    try:
+        return sllm.Comm.nvls(gpus, nbytes, timeout_ms=30000)
+    except sllm.SllmError as ex:
+        assert ex.status == 1, ex          # capability failure is SLLM_E_INVALID, nothing else
+        pytest.skip(f"NVLS multicast not available on this platform: {ex}")
+
+
+def test_nvls_capability_probe_is_clean():
+    """Creating an NVLS group either works or fails with SLLM_E_INVALID naming the driver
+    call -- never a crash or a sticky CUDA error: a plain load still runs afterwards."""
+    try:
+        comms = sllm.Comm.nvls([0], 1 << 20)
+        for c in comms:
+            c.free()
+    except sllm.SllmError as ex:
+        assert ex.status == 1 and "NVLS" in str(ex)
+    inv, seed = models.model_inventory("toy")
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    lay, oparts, _ = oracle_of(inv, seed)
+    res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20))
+    assert np.array_equal(res._keep[3][0].cpu().numpy(), oparts[0])
+
+
+def test_nvls_fanout_needs_an_nvls_group():
+    inv, seed = models.model_inventory("toy")
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    L = idx.partitions[0].length
+    base = torch.empty(L, dtype=torch.uint8, device="cuda")
+    sig = torch.zeros(2, dtype=torch.int32, device="cuda")
+    peers = sllm.Comm.peers(1, 0, 0, [base.data_ptr()], [sig.data_ptr()])
+    with pytest.raises(sllm.SllmError) as ex:    # a P2P peer group has no multicast address
+        sllm.load_start(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, fanout="nvls"), {0: base}, None, None,
+                        peers)
+    assert ex.value.status == 1 and "NVLS" in str(ex.value)
+    peers.free()
+
+
+@pytest.mark.parametrize("mode", ["ce", "zerocopy"])
+def test_nvls_fanout_every_replica_bit_exact(mode):
+    """All visible GPUs (up to 8) in one NVLS group driven by this process: rank r moves its
+    slice over PCIe and its loading kernel stores every vector once through the multicast
+    address; every replica ends equal to P_0, every block checksum to the oracle's, and the
+    group moved each byte over PCIe once."""
+    R = min(NGPU, 8)
+    inv, seed = replicated_inventory(53)
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    lay, oparts, _ = oracle_of(inv, seed)
+    L = idx.partitions[0].length
+    comms = _nvls_or_skip(list(range(R)), L)
+    reps = [c.replica() for c in comms]
+    assert all(r.numel() >= L for r in reps)
+    cfg = sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode, fanout="nvls")
+    for epoch in range(2):
+        for r in range(R):
+            reps[r].fill_(0x6B + epoch)
+            torch.cuda.synchronize(r)
+        results = [sllm.load_start(idx, bufs, {0: r}, cfg, {0: reps[r]}, None, None, comms[r]) for r in range(R)]
+        reports = [res.wait() for res in results]
+        for r in range(R):
+            assert np.array_equal(reps[r][:L].cpu().numpy(), oparts[0]), (epoch, r)
+            assert results[r].block_checksums(0).tolist() == lay.checksums[0]
+            assert reports[r]["fanout_bytes"] == L - reports[r]["transferred_bytes"]
+        assert sum(rep["transferred_bytes"] for rep in reports) == L
+        del results
+    for c in comms:
+        c.free()
