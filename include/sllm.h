@@ -209,6 +209,14 @@ SLLM_API sllm_status sllm_allgather_round(uint64_t length, uint64_t chunk, int32
  * ------------------------------------------------------------------------------------ */
 SLLM_API sllm_status sllm_host_alloc(uint64_t bytes, int32_t gpu, void** p);
 SLLM_API void sllm_host_free(void* p);
+/* NUMA placement: *node = the NUMA node of GPU `gpu`'s PCIe root (sysfs), or -1
+ * when the host does not report one; sllm_host_numa_node: the node holding the page at host
+ * address p (get_mempolicy), -1 if unknown.  The library binds the pages of sllm_host_alloc
+ * (gpu >= 0) to that node, and runs the threads touching them -- first touch, per-partition
+ * load workers, storage readers, converter fill / checksum threads -- on its CPUs when the
+ * host has several nodes. */
+SLLM_API sllm_status sllm_gpu_numa_node(int32_t gpu, int32_t* node);
+SLLM_API sllm_status sllm_host_numa_node(const void* p, int32_t* node);
 /* Page-lock + map caller-owned memory (e.g. a NumPy array) so it can be a load source. */
 SLLM_API sllm_status sllm_host_register(void* p, uint64_t bytes);
 SLLM_API sllm_status sllm_host_unregister(void* p);

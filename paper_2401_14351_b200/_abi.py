@@ -108,6 +108,8 @@ SIGNATURES = {
     "sllm_device_trim": (S, [C.c_int32, U64]),
     "sllm_allgather_round": (S, [U64, U64, C.c_int32, U64, C.POINTER(U64), C.POINTER(U64), C.POINTER(C.c_int32)]),
     "sllm_fanout_unit": (S, [U64, C.c_int32, C.POINTER(U64)]),
+    "sllm_gpu_numa_node": (S, [C.c_int32, C.POINTER(C.c_int32)]),
+    "sllm_host_numa_node": (S, [P, C.POINTER(C.c_int32)]),
     "sllm_host_alloc": (S, [U64, C.c_int32, PP]),
     "sllm_host_free": (None, [P]),
     "sllm_host_register": (S, [P, U64]),

@@ -302,6 +302,20 @@ sllm_status sllm_allgather_round(uint64_t length, uint64_t chunk, int32_t nranks
   });
 }
 
+sllm_status sllm_gpu_numa_node(int32_t gpu, int32_t* node) {
+  return guard([&] {
+    if (!node || gpu < 0) fail(SLLM_E_INVALID, "bad argument");
+    *node = gpu_numa_node(gpu);
+  });
+}
+
+sllm_status sllm_host_numa_node(const void* p, int32_t* node) {
+  return guard([&] {
+    if (!p || !node) fail(SLLM_E_INVALID, "null argument");
+    *node = page_node(p);
+  });
+}
+
 sllm_status sllm_fanout_unit(uint64_t chunk, int32_t fanout, uint64_t* unit) {
   return guard([&] {
     if (!chunk || !unit) fail(SLLM_E_INVALID, "bad fan-out unit arguments");

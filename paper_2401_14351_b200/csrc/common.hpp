@@ -35,6 +35,13 @@ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 int dtype_width(int32_t dtype);  // 0 for unknown codes
 
+// NUMA (numa.cpp)
+int numa_nodes();
+int gpu_numa_node(int gpu);            // -1 if unknown
+bool bind_thread_to_node(int node);    // calling thread -> that node's CPUs (multi-node hosts)
+bool bind_thread_to_gpu(int gpu);      // ... the node of `gpu`'s PCIe root
+int page_node(const void* p);          // node holding the page at p, -1 if unknown
+
 struct TensorRec {
   std::string name;
   int32_t device;

@@ -85,6 +85,7 @@ static void read_window(FileSource& f, uint64_t w, uint8_t* dst) {
 static void io_main(FileSource* f, int gpu) {
   try {
     cudaSetDevice(gpu);
+    bind_thread_to_gpu(gpu);  // readers fill slots on the GPU's node
     for (;;) {
       const uint64_t w = f->next.fetch_add(1);
       if (w >= f->nwin || f->stop) return;

@@ -87,10 +87,18 @@ static void parallel_for(size_t n, int threads, F fn) {
   auto body = [&] {
     for (size_t i; (i = next.fetch_add(1)) < n;) fn(i);
   };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < threads; ++t) pool.emplace_back(body);
-  body();
+  std::vector<std::thread> pool;  // (worker threads only: jobs may re-bind their thread's NUMA affinity)
+  for (int t = 0; t < threads; ++t) pool.emplace_back(body);
   for (auto& th : pool) th.join();
+}
+
+// Converter threads fill / checksum a partition's pinned buffer from the CPUs of the node its
+// pages live on (numa.cpp; no-op on single-node hosts).
+static void follow_pages(const void* buf) {
+  static thread_local const void* last = nullptr;
+  if (numa_nodes() <= 1 || buf == last) return;
+  last = buf;
+  bind_thread_to_node(page_node(buf));
 }
 
 // ---------------------------------------------------------------------------------
@@ -196,6 +204,7 @@ void seal(sllm_index* idx, const void* const* part_bufs) {
       const PartRec& pr = idx->parts[jobs[i].p];
       uint64_t lo = jobs[i].j * idx->block;
       uint64_t len = std::min(idx->block, pr.length - lo);
+      follow_pages(part_bufs[jobs[i].p]);
       idx->parts[jobs[i].p].checksums[jobs[i].j] =
           fletcher64(static_cast<const uint8_t*>(part_bufs[jobs[i].p]) + lo, len);
     });
@@ -227,6 +236,7 @@ void convert_into(const sllm_src_tensor* t, size_t n, sllm_index* idx, void* con
   parallel_for(jobs.size(), default_threads(), [&](size_t i) {
     PartRec& pr = idx->parts[jobs[i].p];
     uint8_t* base = static_cast<uint8_t*>(part_bufs[jobs[i].p]);
+    follow_pages(base);
     const uint64_t lo = jobs[i].j * B, hi = std::min(lo + B, pr.length);
     // first tensor (in offset order) that ends after lo
     auto it = std::partition_point(pr.by_offset.begin(), pr.by_offset.end(), [&](uint32_t ti) {

@@ -80,6 +80,7 @@ void gds_read(const std::string& path, int gpu, uint8_t* dst, uint64_t lo, uint6
   bool failed = false;
   auto reader = [&] {
     cudaSetDevice(gpu);
+    bind_thread_to_gpu(gpu);
     for (;;) {
       const uint64_t w = next.fetch_add(1);
       if (w >= nwin) return;

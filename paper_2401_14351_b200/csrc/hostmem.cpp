@@ -25,48 +25,20 @@ struct HostAlloc {
 static std::mutex g_host_mu;
 static std::map<void*, HostAlloc> g_host;
 
-static int gpu_numa_node(int gpu) {
-  char bus[32] = {};
-  if (cudaDeviceGetPCIBusId(bus, sizeof bus, gpu) != cudaSuccess) {
-    cudaGetLastError();
-    return -1;
-  }
-  std::string b(bus);
-  for (auto& ch : b) ch = (char)tolower(ch);
-  // cudaDeviceGetPCIBusId returns "0000:d1:00.0"; sysfs uses the same form
-  std::string path = "/sys/bus/pci/devices/" + b + "/numa_node";
-  FILE* f = fopen(path.c_str(), "r");
-  if (!f) return -1;
-  int node = -1;
-  if (fscanf(f, "%d", &node) != 1) node = -1;
-  fclose(f);
-  return node;
-}
-
-static int numa_nodes() {
-  int n = 0;
-  for (int i = 0; i < 1024; ++i) {
-    std::string p = "/sys/devices/system/node/node" + std::to_string(i);
-    if (access(p.c_str(), F_OK) != 0) break;
-    ++n;
-  }
-  return n;
-}
-
-static void parallel_touch(uint8_t* p, uint64_t bytes) {
+static void parallel_touch(uint8_t* p, uint64_t bytes, int node) {
   const uint64_t piece = 64ull << 20;
   uint64_t n = ceil_div(bytes, piece);
   int threads = (int)std::min<uint64_t>(n, (uint64_t)default_threads());
   std::vector<std::thread> th;
   std::atomic<uint64_t> next{0};
   auto body = [&] {
+    bind_thread_to_node(node);  // first touch from the node the pages are bound to
     for (uint64_t i; (i = next.fetch_add(1)) < n;) {
       uint64_t lo = i * piece, len = std::min(piece, bytes - lo);
       std::memset(p + lo, 0, len);
     }
   };
-  for (int t = 1; t < threads; ++t) th.emplace_back(body);
-  body();
+  for (int t = 0; t < threads; ++t) th.emplace_back(body);  // (the caller's own affinity stays)
   for (auto& t : th) t.join();
 }
 
@@ -76,14 +48,15 @@ void* host_alloc(uint64_t bytes, int gpu) {
   void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
   if (p != MAP_FAILED) {
     madvise(p, len, MADV_HUGEPAGE);
+    int node = -1;
     if (gpu >= 0 && numa_nodes() > 1) {
-      int node = gpu_numa_node(gpu);
+      node = gpu_numa_node(gpu);
       if (node >= 0 && node < 64) {
         unsigned long mask = 1ul << node;
         syscall(SYS_mbind, p, len, 2 /*MPOL_BIND*/, &mask, 64, 0);
       }
     }
-    parallel_touch(static_cast<uint8_t*>(p), len);
+    parallel_touch(static_cast<uint8_t*>(p), len, node);
     cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable);
     if (e == cudaSuccess) {
       std::lock_guard<std::mutex> g(g_host_mu);

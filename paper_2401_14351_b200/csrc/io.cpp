@@ -102,7 +102,9 @@ void read_partition(const char* dir, const sllm_index* idx, size_t p, void* dst,
   threads = (int)std::min<uint64_t>((uint64_t)threads, std::max<uint64_t>(nch, 1));
   std::atomic<uint64_t> next{0};
   std::atomic<int> err{0};
+  const int node = page_node(dst);  // readers run on the node of the destination pages
   auto body = [&] {
+    bind_thread_to_node(node);
     for (uint64_t k; (k = next.fetch_add(1)) < nch && !err.load();) {
       uint64_t lo = k * kChunk, hi = std::min(lo + kChunk, pr.length);
       while (lo < hi) {
@@ -118,8 +120,7 @@ void read_partition(const char* dir, const sllm_index* idx, size_t p, void* dst,
     }
   };
   std::vector<std::thread> th;
-  for (int t = 1; t < threads; ++t) th.emplace_back(body);
-  body();
+  for (int t = 0; t < threads; ++t) th.emplace_back(body);  // (never re-binds the caller)
   for (auto& t : th) t.join();
   if (fd_dir >= 0) ::close(fd_dir);
   ::close(fd_buf);

@@ -499,6 +499,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   const PartRec& pr = idx.parts[j.p];
   const uint64_t t0 = now_ns();
   SLLM_CUDA(cudaSetDevice(j.gpu));
+  bind_thread_to_gpu(j.gpu);  // the worker runs next to its GPU's PCIe root and pinned pages
   DeviceCtx& dc = device_ctx(j.gpu);
   {
     std::lock_guard<std::mutex> g(dc.mu);
