@@ -822,7 +822,7 @@ def main(argv=None):
                 ("checksum only" if args.mode == "ce" else "scatter+checksum"),
                 "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
                 "bytes_per_launch": per_launch_bytes,
-                "note": "one CTA per SM; each launch verifies a span of landed windows (up to 2 GiB, halving towards the end) "
+                "note": "one CTA per SM; each launch verifies a span of landed windows (up to 4 GiB, halving towards the end) "
                         "(1 MiB blocks split into equal units for wave balance) beside the PCIe copies"}
     if args.mode in ("zerocopy", "scatter_zc") and kern_launches and kern_ms > 0:
         # zero-copy kernel: every byte it reads crosses PCIe -> bound by the host link.

@@ -40,9 +40,8 @@ void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint6
   uint8_t* b = static_cast<uint8_t*>(scratch);
   Seg* seg = reinterpret_cast<Seg*>(b + acc_bytes);
   unsigned long long* bad = reinterpret_cast<unsigned long long*>(b + acc_bytes + 128);
-  Seg h{0, len, nullptr, 0};
   SLLM_CUDA(cudaMemsetAsync(b, 0, acc_bytes, st));
-  SLLM_CUDA(cudaMemcpyAsync(seg, &h, sizeof h, cudaMemcpyHostToDevice, st));
+  SLLM_CUDA(launch_init_seg(seg, len, st));  // (a pageable upload would synchronise the stream)
   MatParams mp{};
   mp.src = static_cast<const uint8_t*>(src);
   mp.lo = 0;

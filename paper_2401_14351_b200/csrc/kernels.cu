@@ -515,6 +515,13 @@ __global__ void peer_wait_kernel(const uint32_t* own, int nranks, int me, uint32
   }
 }
 
+__global__ void init_seg_kernel(Seg* seg, uint64_t len) { *seg = Seg{0, len, nullptr, 0}; }
+
+cudaError_t launch_init_seg(Seg* seg, uint64_t len, cudaStream_t stream) {
+  init_seg_kernel<<<1, 1, 0, stream>>>(seg, len);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_peer_signal(const PeerSignal& s, uint32_t epoch, cudaStream_t stream) {
   if (!s.n) return cudaSuccess;
   peer_signal_kernel<<<1, 32, 0, stream>>>(s, epoch);
@@ -552,6 +559,11 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
     cudaError_t e = cudaFuncSetAttribute(materialise_tma_kernel<kStore, kCheck>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     if (e != cudaSuccess) return e;
+#ifdef SLLM_SMEM_CARVEOUT  // A/B knob: fix the L1/shared split (percent shared) for the ring kernels
+    e = cudaFuncSetAttribute(materialise_tma_kernel<kStore, kCheck>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             SLLM_SMEM_CARVEOUT);
+    if (e != cudaSuccess) return e;
+#endif
     configured[dev & 63].store(true, std::memory_order_release);
   }
   // Split checksum blocks into up to 16 units of >= one stage (16 KiB) while the launch

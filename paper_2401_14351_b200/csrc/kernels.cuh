@@ -80,6 +80,9 @@ struct PeerSignal {
   uint32_t n;
 };
 cudaError_t launch_peer_signal(const PeerSignal& s, uint32_t epoch, cudaStream_t stream);
+// Write the single whole-buffer segment {0, len, null, 0} of a device-resident checksum
+// pass (no host staging copy on the stream: a pageable upload would synchronise it).
+cudaError_t launch_init_seg(Seg* seg, uint64_t len, cudaStream_t stream);
 cudaError_t launch_peer_wait(const uint32_t* own, int nranks, int me, uint32_t epoch, uint64_t timeout_ns,
                              uint32_t* err, cudaStream_t stream);
 
