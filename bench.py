@@ -68,10 +68,12 @@ def parse(argv=None):
     ap.add_argument("--spread", action="store_true",
                     help="with --all-partitions: partition p on GPU p %% (visible GPUs), all from this one process -- "
                          "the paper's model manager loading every GPU of a server (P:721-727)")
-    ap.add_argument("--fanout", default="none", choices=["none", "bcast", "allgather", "p2p"],
+    ap.add_argument("--fanout", default="none", choices=["none", "bcast", "allgather", "p2p", "nvls"],
                     help="replicated checkpoint: every rank ends with a full replica; rank r reads slice r over "
                          "PCIe and the rest arrives over NVLink (bcast: NCCL broadcasts, allgather: in-place NCCL "
-                         "all-gathers, p2p: fused peer stores)")
+                         "all-gathers, p2p: fused peer stores, nvls: multicast stores from ONE process over "
+                         "--nvls-gpus GPUs)")
+    ap.add_argument("--nvls-gpus", type=int, default=0, help="--fanout nvls: group size (0 = every visible GPU)")
     ap.add_argument("--cpu-sample-gib", type=float, default=2.0,
                     help="oracle sample per partition (cpu_baseline and --impl reference)")
     ap.add_argument("--cpu-reps", type=int, default=3, help="timed oracle reps for cpu_baseline")
@@ -622,6 +624,98 @@ def replicated_baselines(sllm, torch, idx, bufs, gpus, cfg, bases, world, rank, 
     return out
 
 
+def run_nvls(args):
+    """Replicated checkpoint over an NVLS multicast group driven by this one process (SURVEY
+    §8(f) rank 4; the paper's model manager loading every GPU of a server): R GPUs,
+    rank r reads slice r over its own PCIe link, its loading kernel stores every vector once
+    through the multicast address and the NVSwitch writes all R replicas.  Fails loudly
+    (exit 2) where the platform cannot create multicast objects."""
+    import torch
+    import paper_2401_14351_b200 as sllm
+    from paper_2401_14351_b200 import workloads
+    from synth import models, payload
+    payload.build_csynth()
+    R = args.nvls_gpus or visible_gpus()
+    if R < 1 or visible_gpus() < R:
+        fail_loudly(f"--fanout nvls over {R} GPUs needs {R} visible GPUs, found {visible_gpus()}")
+    config = args.config if args.config != "auto" else REPLICATED_CONFIG
+    inv, seed = models.model_inventory(config)
+    if len(set(t.device for t in inv)) != 1:
+        fail_loudly("--fanout nvls needs a single-partition (replicated) checkpoint config")
+    t0 = time.perf_counter()
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, config, partitions=[0], gpu_of={0: 0})
+    t_setup = time.perf_counter() - t0
+    blob = idx.serialize()
+    L = idx.partitions[0].length
+    payload_bytes = sum(t.nbytes for t in idx.tensors)
+    try:
+        comms = sllm.Comm.nvls(list(range(R)), L)
+    except sllm.SllmError as ex:
+        fail_loudly(f"NVLS unavailable on this platform: {ex}")
+    bases = [c.replica()[:L] for c in comms]
+    cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, n_streams=args.streams, mode=args.mode,
+                          ctas=args.ctas, fanout="nvls", engine=args.engine)
+    streams = [torch.cuda.current_stream(r) for r in range(R)]
+    # B_h2d(R): every GPU copies 4 GiB of the partition at once (the R links together)
+    n = min(4 << 30, L)
+    best = 0.0
+    for _ in range(3):
+        for r in range(R):
+            torch.cuda.synchronize(r)
+        evs = []
+        for r in range(R):
+            with torch.cuda.device(r):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                bases[r][:n].copy_(bufs[0].torch()[:n], non_blocking=True)
+                b.record()
+                evs.append((a, b))
+        for a, b in evs:
+            b.synchronize()
+        best = max(best, R * n / (max(a.elapsed_time(b) for a, b in evs) * 1e-3) / 1e9)
+
+    def step():
+        ix = sllm.Index.from_bytes(blob)
+        results = [sllm.load_start(ix, bufs, {0: r}, cfg, {0: bases[r]}, None, {0: streams[r]}, comms[r])
+                   for r in range(R)]
+        return [res.wait() for res in results]
+    for _ in range(args.warmup):
+        step()
+    for r in range(R):
+        torch.cuda.synchronize(r)
+    marks = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(R)]
+             for _ in range(args.steps)]
+    reports = []
+    with ClockSampler(0) as clk:
+        for k in range(args.steps):
+            for r in range(R):
+                marks[k][r][0].record(streams[r])
+            reports = step()
+            for r in range(R):
+                marks[k][r][1].record(streams[r])
+        for r in range(R):
+            torch.cuda.synchronize(r)
+    ms_steps = [max(m[r][0].elapsed_time(m[r][1]) for r in range(R)) for m in marks]
+    ms_step = max(marks[0][r][0].elapsed_time(marks[-1][r][1]) for r in range(R)) / args.steps
+    ok = all(c.replica()[:L].cpu().numpy().tobytes() == bufs[0].numpy()[:L].tobytes() for c in comms[:1])
+    pcie = sum(rep["transferred_bytes"] for rep in reports)
+    value = payload_bytes * R / (ms_step * 1e-3) / 1e9
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": R, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": arm_config(args, config, R, 1, payload_bytes, L, True,
+                                 {"nvls": f"one process, multicast group over GPUs 0..{R - 1}"}),
+            "time_to_loaded_model_s": ms_step * 1e-3, "step_ms": step_stats(ms_steps), "t_setup_s": t_setup,
+            "b_h2d_measured_GBps": best, "frac_h2d": pcie / (ms_step * 1e-3) / 1e9 / best,
+            "roofline_h2d": {"bound": "pcie", "achieved": pcie / (ms_step * 1e-3) / 1e9, "peak": best, "unit": "GB/s",
+                             "frac": pcie / (ms_step * 1e-3) / 1e9 / best, "n_links": R},
+            "replica0_equals_source": ok, "gpu_launches": sum(int(rep["kernel_launches"]) for rep in reports) * args.steps,
+            "clocks": clk.summary(), "e2e": None, "roofline": None, "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
+    for c in comms:
+        c.free()
+
+
 def main(argv=None):
     argv = sys.argv[1:] if argv is None else argv
     args = parse(argv)
@@ -637,6 +731,11 @@ def main(argv=None):
             import torch.distributed as dist
             dist.init_process_group("gloo")
         run_plumbing(args, rank, world, local)
+        return
+    if args.fanout == "nvls":
+        if world > 1:
+            fail_loudly("--fanout nvls drives every GPU of the group from one process: run without torchrun")
+        run_nvls(args)
         return
     import torch
     if world > 1:

@@ -320,3 +320,19 @@ def test_nvls_fanout_every_replica_bit_exact(mode):
         del results
     for c in comms:
         c.free()
+
+
+def test_bench_nvls_fails_loudly_or_runs():
+    """`bench.py --fanout nvls` either measures the multicast group or exits 2 naming why the
+    platform has no NVLS -- never a silent fallback to another fan-out."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--fanout", "nvls", "--config", "toy",
+                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=root)
+    if out.returncode == 0:
+        line = json.loads(out.stdout.strip().splitlines()[-1])
+        assert line["replica0_equals_source"] and line["config"]["fanout"] == "nvls"
+    else:
+        assert out.returncode == 2 and "NVLS unavailable" in out.stderr, out.stderr[-2000:]
