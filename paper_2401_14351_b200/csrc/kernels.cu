@@ -284,7 +284,9 @@ __device__ __forceinline__ uint32_t find_seg(const MatParams& p, uint64_t a) {
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory"); }
 
-template <bool kStore, bool kCheck>
+// kMc: the NVLS fan-out's instance (every vector stored once through the multicast address;
+// a separate instance keeps the per-vector test out of the K2 / K3 store loops)
+template <bool kStore, bool kCheck, bool kMc = false>
 __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const MatParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kStageBytes);
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   // engine 2: the tensor bytes leave shared memory by TMA bulk stores issued by one
   // storer thread (contiguous pieces: segment x stage); consumers then only read smem for
   // the checksum and write the < 16-byte tails of tensors.
-  const bool bulk_store = kStore && p.engine == 2 && p.n_peers == 0 && !p.mc && !p.no_seg_store;
+  const bool bulk_store = kStore && !kMc && p.engine == 2 && p.n_peers == 0 && !p.no_seg_store;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
       for (uint32_t v = (uint32_t)ct * 16; v < n; v += 32 * kConsumerWarps * 16) {
         const uint4 val = lds16(sb + v);
         const uint64_t x = off + v;
-        if (kStore && p.mc) {
+        if (kMc) {
           mc_store16(p.mc + x, val);  // NVLS fan-out (contiguous): every replica at once
         } else if (kStore) {
           while (x >= sg.off + sg.len && cur + 1 < p.seg_end) sg = p.segs[++cur];
@@ -548,7 +550,7 @@ static int num_sms() {
   return sms;
 }
 
-template <bool kStore, bool kCheck>
+template <bool kStore, bool kCheck, bool kMc = false>
 static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream) {
   // The dynamic shared-memory opt-in is a property of the kernel in each device's context:
   // set it once per (template instance, device); worker threads of different GPUs race here.
@@ -556,12 +558,12 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
   int dev = 0;
   cudaGetDevice(&dev);
   if (!configured[dev & 63].load(std::memory_order_acquire)) {
-    cudaError_t e = cudaFuncSetAttribute(materialise_tma_kernel<kStore, kCheck>,
+    cudaError_t e = cudaFuncSetAttribute(materialise_tma_kernel<kStore, kCheck, kMc>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     if (e != cudaSuccess) return e;
 #ifdef SLLM_SMEM_CARVEOUT  // A/B knob: fix the L1/shared split (percent shared) for the ring kernels
-    e = cudaFuncSetAttribute(materialise_tma_kernel<kStore, kCheck>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             SLLM_SMEM_CARVEOUT);
+    e = cudaFuncSetAttribute(materialise_tma_kernel<kStore, kCheck, kMc>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, SLLM_SMEM_CARVEOUT);
     if (e != cudaSuccess) return e;
 #endif
     configured[dev & 63].store(true, std::memory_order_release);
@@ -594,7 +596,7 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
   const uint64_t unit = blk / q.split;
   const uint64_t units = (p.hi + unit - 1) / unit - p.lo / unit;
   if ((uint64_t)grid > units) grid = (int)units;
-  materialise_tma_kernel<kStore, kCheck><<<grid, kTmaThreads, kTmaSmem, stream>>>(q);
+  materialise_tma_kernel<kStore, kCheck, kMc><<<grid, kTmaThreads, kTmaSmem, stream>>>(q);
   return cudaGetLastError();
 }
 
@@ -604,8 +606,10 @@ cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaS
   if (p.engine >= 1) {
     switch (kind) {
       case MatKind::kChecksumOnly: return launch_tma<false, true>(p, grid, stream);
-      case MatKind::kCopyChecksum: return launch_tma<true, true>(p, grid, stream);
-      case MatKind::kCopyOnly: return launch_tma<true, false>(p, grid, stream);
+      case MatKind::kCopyChecksum:
+        return p.mc ? launch_tma<true, true, true>(p, grid, stream) : launch_tma<true, true>(p, grid, stream);
+      case MatKind::kCopyOnly:
+        return p.mc ? launch_tma<true, false, true>(p, grid, stream) : launch_tma<true, false>(p, grid, stream);
     }
   }
   const uint64_t ntiles = (p.hi - p.lo + p.tile - 1) / p.tile;
