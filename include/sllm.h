@@ -186,7 +186,7 @@ SLLM_API sllm_status sllm_replica_round(uint64_t length, uint64_t chunk, int32_t
                                         uint64_t* lo_hi, uint64_t* n_rounds);
 /* Unit of the NCCL fan-outs' slices and rounds for a load with chunk size `chunk` and fan-out
  * `fanout`: BCAST / ALLGATHER slice the partition and run their rounds in whole copy windows
- * of chunks (max(1, 64 MiB / chunk) chunks -- one batched copy submission and one grouped
+ * of chunks (max(1, 64 MiB / chunk) chunks -- one copy submission and one grouped
  * broadcast / all-gather per round instead of one per chunk); every other fan-out: `chunk`.
  * The loader calls sllm_replica_slices / sllm_replica_round / sllm_allgather_round with this
  * unit in place of the chunk. */

@@ -40,7 +40,8 @@ void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint6
   uint8_t* b = static_cast<uint8_t*>(scratch);
   Seg* seg = reinterpret_cast<Seg*>(b + acc_bytes);
   unsigned long long* bad = reinterpret_cast<unsigned long long*>(b + acc_bytes + 128);
-  SLLM_CUDA(cudaMemsetAsync(b, 0, acc_bytes, st));
+  unsigned long long* ticket = reinterpret_cast<unsigned long long*>(b + acc_bytes + 256);
+  SLLM_CUDA(cudaMemsetAsync(b, 0, acc_bytes + 512, st));
   SLLM_CUDA(launch_init_seg(seg, len, st));  // (a pageable upload would synchronise the stream)
   MatParams mp{};
   mp.src = static_cast<const uint8_t*>(src);
@@ -56,6 +57,7 @@ void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint6
   mp.cs_out = out;
   mp.bad = bad;
   mp.engine = standalone_engine();
+  if (!getenv("SLLM_STATIC_UNITS")) mp.ticket = ticket;  // dynamic unit distribution (base 0)
   SLLM_CUDA(launch_materialise(mp, MatKind::kChecksumOnly, ctas > 0 ? ctas : default_grid(), st));
   SLLM_CUDA(cudaFreeAsync(scratch, st));
 }
@@ -85,13 +87,15 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   gran_table(segs, pr.length, kGranShift, gran);
   const size_t gran_bytes = align_up(gran.size() * 4, 256);
   void* scratch = nullptr;
-  SLLM_CUDA(cudaMallocAsync(&scratch, seg_bytes + acc_bytes + tab + 256 + gran_bytes, st));
+  SLLM_CUDA(cudaMallocAsync(&scratch, seg_bytes + acc_bytes + tab + 256 + gran_bytes + 256, st));
   uint8_t* b = static_cast<uint8_t*>(scratch);
   Seg* d_segs = reinterpret_cast<Seg*>(b);
   BlockAcc* d_acc = reinterpret_cast<BlockAcc*>(b + seg_bytes);
   uint64_t* d_expect = reinterpret_cast<uint64_t*>(b + seg_bytes + acc_bytes);
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(b + seg_bytes + acc_bytes + tab);
   uint32_t* d_gran = reinterpret_cast<uint32_t*>(b + seg_bytes + acc_bytes + tab + 256);
+  unsigned long long* d_ticket = reinterpret_cast<unsigned long long*>(b + seg_bytes + acc_bytes + tab + 256 + gran_bytes);
+  SLLM_CUDA(cudaMemsetAsync(d_ticket, 0, 8, st));
   SLLM_CUDA(cudaMemcpyAsync(d_gran, gran.data(), gran.size() * 4, cudaMemcpyHostToDevice, st));
   SLLM_CUDA(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice, st));
   SLLM_CUDA(cudaMemsetAsync(d_acc, 0, acc_bytes, st));
@@ -114,6 +118,7 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   mp.expect = check ? d_expect : nullptr;
   mp.bad = d_bad;
   mp.engine = standalone_engine();
+  if (!getenv("SLLM_STATIC_UNITS")) mp.ticket = d_ticket;  // dynamic unit distribution (base 0)
   cudaEvent_t ev[2] = {};
   if (kernel_ms)
     for (auto& e : ev) SLLM_CUDA(cudaEventCreate(&e));

@@ -204,12 +204,6 @@ constexpr int kStoreLag = 4;                             // bulk-store groups in
 #define SLLM_STAGE_KIB 16
 #endif
 constexpr int kConsumerUnroll = SLLM_CONSUMER_UNROLL;
-// Lanes of the producer warp issuing bulk copies (A/B knob: "several producer
-// lanes" for the zero-copy host reads; profiles/r02/zc_ab.jsonl)
-#ifndef SLLM_PRODUCER_LANES
-#define SLLM_PRODUCER_LANES 1
-#endif
-constexpr int kProducerLanes = SLLM_PRODUCER_LANES;
 constexpr uint32_t kStageBytes = SLLM_STAGE_KIB << 10;  // ring: kStages x kStageBytes = 192 KiB
 constexpr int kStages = (192 << 10) / kStageBytes;
 constexpr uint64_t kMaxUnitBytes = 1ull << 20;  // default: whole 1 MiB blocks when the launch is balanced
@@ -282,6 +276,24 @@ __device__ __forceinline__ uint32_t find_seg(const MatParams& p, uint64_t a) {
   return lo;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ktime_mark(unsigned long long* kt, int which) {
+  const unsigned long long t = globaltimer();
+  atomicMax(kt + 2 * which, ~t);
+  atomicMax(kt + 2 * which + 1, t);
+}
+
+constexpr uint64_t kNoUnit = ~0ull;
+// The unit index the producer stored for a stage, read after that stage's full-barrier wait
+// (acquire) -- volatile so the compiler cannot hoist it above the wait.
+__device__ __forceinline__ uint64_t unit_of(const uint64_t* s_unit, uint32_t stage) {
+  return *static_cast<const volatile uint64_t*>(s_unit + stage);
+}
+
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory"); }
 
 // kMc: the NVLS fan-out's instance (every vector stored once through the multicast address;
@@ -292,6 +304,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   __shared__ unsigned long long s_red[2][3][kConsumerWarps];  // double-buffered by unit parity
+  __shared__ uint64_t s_unit[kStages];  // unit whose first stage is in the slot (kNoUnit: end)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Work unit: a 1/split-th of a checksum block (a CTA owns whole units).  split > 1 lets
   // a launch covering few blocks still spread over every SM; the partial sums of a
@@ -299,6 +312,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   const uint64_t blk = kCheck ? p.block : (1ull << 20);
   const uint64_t unit = blk / p.split;
   const uint64_t u_first = p.lo / unit, u_end = (p.hi + unit - 1) / unit;
+  if (p.ktime && threadIdx.x == 0) ktime_mark(p.ktime, 0);
 
   // engine 2: the tensor bytes leave shared memory by TMA bulk stores issued by one
   // storer thread (contiguous pieces: segment x stage); consumers then only read smem for
@@ -314,26 +328,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   }
   __syncthreads();
 
-  if (warp == 0) {  // producer (kProducerLanes lanes issue the stages round-robin; default 1)
-    if (lane < kProducerLanes) {
-      uint32_t stage = 0, phase = 0, seq = 0;
-      for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x) {
+  if (warp == 0) {  // producer: picks the CTA's units and streams them through the ring
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      uint64_t u = u_first + blockIdx.x;  // first unit: static (grid <= units)
+      for (;;) {
         const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
-        for (uint64_t off = a; off < e; off += kStageBytes, ++seq) {
-          if (kProducerLanes > 1 && seq % kProducerLanes != (uint32_t)lane) {
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
-            continue;
-          }
+        for (uint64_t off = a; off < e; off += kStageBytes) {
           const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
           mbar_wait(&empty[stage], phase ^ 1);
           // the consumers' generic-proxy reads of this stage (ordered before their empty
           // arrivals) happen before the async-proxy TMA write that refills it
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (off == a) s_unit[stage] = u;  // published by the arrive below (release)
           mbar_expect_tx(&full[stage], n);
           bulk_g2s(smem + (size_t)stage * kStageBytes, p.src + (off - p.src_origin), n, &full[stage]);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+        // next unit: dynamic (a ticket, drawn once this unit is fully issued -- the ring
+        // still holds up to 12 stages for the consumers, which hides the atomic) or static
+        u = p.ticket ? u_first + gridDim.x + (atomicAdd(p.ticket, 1ull) - p.ticket_base) : u + gridDim.x;
+        if (u >= u_end) break;
       }
+      mbar_wait(&empty[stage], phase ^ 1);
+      s_unit[stage] = kNoUnit;  // end of the CTA's work: a stage with no bytes
+      mbar_arrive(&full[stage]);
     }
     return;
   }
@@ -343,13 +362,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
       uint32_t stage = 0, phase = 0;
       uint32_t ring[kStoreLag + 1];
       int head = 0, cnt = 0;  // stages whose stores may still read smem, oldest first
-      for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x) {
+      for (;;) {
+        mbar_wait(&full[stage], phase);
+        const uint64_t u = unit_of(s_unit, stage);
+        if (u == kNoUnit) break;
         const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
         uint32_t cur = find_seg(p, a);
         Seg sg = p.segs[cur];
         for (uint64_t off = a; off < e; off += kStageBytes) {
           const uint64_t end = off + min((uint64_t)kStageBytes, e - off);
-          mbar_wait(&full[stage], phase);
+          if (off != a) mbar_wait(&full[stage], phase);
           const uint8_t* sb = smem + (size_t)stage * kStageBytes;
           while (off >= sg.off + sg.len && cur + 1 < p.seg_end) sg = p.segs[++cur];
           uint32_t k = cur;
@@ -381,7 +403,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   const int ct = threadIdx.x - 32;  // consumer thread 0..255
   const int cw = warp - 1;
   uint32_t stage = 0, phase = 0, par = 0;
-  for (uint64_t u = u_first + blockIdx.x; u < u_end; u += gridDim.x, par ^= 1) {
+  for (;; par ^= 1) {
+    mbar_wait(&full[stage], phase);  // first stage of the CTA's next unit (or the end mark)
+    const uint64_t u = unit_of(s_unit, stage);
+    if (u == kNoUnit) break;
     const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
     // segment holding byte a (same search in every thread: uniform, L1-cached)
     uint32_t cur = p.seg_begin;
@@ -392,7 +417,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
     for (uint64_t off = a; off < e; off += kStageBytes) {
       const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
       const uint32_t w0 = (uint32_t)((off - bstart) >> 2);  // block word index of the stage start
-      mbar_wait(&full[stage], phase);
+      if (off != a) mbar_wait(&full[stage], phase);
       const uint8_t* sb = smem + (size_t)stage * kStageBytes;
 #pragma unroll kConsumerUnroll
       for (uint32_t v = (uint32_t)ct * 16; v < n; v += 32 * kConsumerWarps * 16) {
@@ -484,6 +509,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
       }
     }
   }
+  if (p.ktime) {  // diagnostic: this CTA's consumers are done
+    consumer_sync();
+    if (ct == 0) ktime_mark(p.ktime, 1);
+  }
 }
 
 }  // namespace
@@ -551,7 +580,7 @@ static int num_sms() {
 }
 
 template <bool kStore, bool kCheck, bool kMc = false>
-static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream) {
+static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream, uint64_t* tickets) {
   // The dynamic shared-memory opt-in is a property of the kernel in each device's context:
   // set it once per (template instance, device); worker threads of different GPUs race here.
   static std::atomic<bool> configured[64];
@@ -596,20 +625,22 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream)
   const uint64_t unit = blk / q.split;
   const uint64_t units = (p.hi + unit - 1) / unit - p.lo / unit;
   if ((uint64_t)grid > units) grid = (int)units;
+  if (tickets) *tickets = q.ticket ? units : 0;  // each CTA draws one ticket past the end
   materialise_tma_kernel<kStore, kCheck, kMc><<<grid, kTmaThreads, kTmaSmem, stream>>>(q);
   return cudaGetLastError();
 }
 
-cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream) {
+cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream, uint64_t* tickets) {
+  if (tickets) *tickets = 0;
   if (p.hi <= p.lo) return cudaSuccess;
   if (grid < 1) grid = num_sms();  // default: one CTA per SM
   if (p.engine >= 1) {
     switch (kind) {
-      case MatKind::kChecksumOnly: return launch_tma<false, true>(p, grid, stream);
+      case MatKind::kChecksumOnly: return launch_tma<false, true>(p, grid, stream, tickets);
       case MatKind::kCopyChecksum:
-        return p.mc ? launch_tma<true, true, true>(p, grid, stream) : launch_tma<true, true>(p, grid, stream);
+        return p.mc ? launch_tma<true, true, true>(p, grid, stream, tickets) : launch_tma<true, true>(p, grid, stream, tickets);
       case MatKind::kCopyOnly:
-        return p.mc ? launch_tma<true, false, true>(p, grid, stream) : launch_tma<true, false>(p, grid, stream);
+        return p.mc ? launch_tma<true, false, true>(p, grid, stream, tickets) : launch_tma<true, false>(p, grid, stream, tickets);
     }
   }
   const uint64_t ntiles = (p.hi - p.lo + p.tile - 1) / p.tile;

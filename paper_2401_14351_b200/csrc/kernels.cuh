@@ -59,6 +59,17 @@ struct MatParams {
   // NVLS fan-out: multicast address of partition byte 0 -- every vector is stored once with
   // multimem.st and lands in every replica of the group (own included); no per-segment store
   uint8_t* mc;
+  // diagnostic (profile dumps with SLLM_KTIME=1, else nullptr): 4 words per launch, zeroed
+  // before it -- [0] = ~min CTA start, [1] = max CTA start, [2] = ~min CTA end, [3] = max
+  // CTA end (%globaltimer ns; the complements let one atomicMax serve min and max)
+  unsigned long long* ktime;
+  // TMA engine work distribution: nullptr = static (CTA b takes units b, b + grid, ...);
+  // else CTA b takes unit b first and then unit grid + (atomicAdd(ticket, 1) - ticket_base)
+  // until that is past the launch's last unit.  Every launch draws exactly `units` tickets
+  // (each CTA draws one past the end), so consecutive launches on one stream share one
+  // counter by advancing ticket_base (launch_materialise reports the count).
+  unsigned long long* ticket;
+  unsigned long long ticket_base;
 };
 
 enum class MatKind : int {
@@ -67,8 +78,10 @@ enum class MatKind : int {
   kCopyOnly = 2        // K2/K3 with verify off
 };
 
-// Launch on `stream` with `grid` CTAs (grid-stride over tiles).  Returns cudaGetLastError().
-cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream);
+// Launch on `stream` with `grid` CTAs.  Returns cudaGetLastError(); *tickets (optional) =
+// tickets the launch draws from p.ticket (0 when it does not use one).
+cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream,
+                               uint64_t* tickets = nullptr);
 
 // P2P fan-out completion: publish `epoch` into one slot of every peer's
 // signal array (system-scope release, after every store of the preceding kernels), and

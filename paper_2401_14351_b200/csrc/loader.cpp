@@ -131,6 +131,11 @@ struct PartJob {
   uint64_t* d_expect = nullptr;
   uint64_t* d_cs = nullptr;
   unsigned long long* d_bad = nullptr;
+  unsigned long long* d_ktime = nullptr;  // diagnostic (SLLM_KTIME + profile): MatParams.ktime slots
+  // dynamic unit distribution (MatParams.ticket): one zeroed counter per launching stream,
+  // with the tickets its earlier launches drew (launches on one stream run in order)
+  unsigned long long* d_tickets = nullptr;
+  std::vector<std::pair<cudaStream_t, uint64_t>> ticket_base;
   cudaEvent_t ev[4] = {};  // start, end, setup, origin
   // results
   std::vector<uint64_t> h_cs;
@@ -234,22 +239,35 @@ static void timed_end(std::pair<cudaEvent_t, cudaEvent_t> e, std::vector<std::pa
   out.push_back(e);
 }
 
-static void launch(PartJob& j, bool prof, const MatParams& mp, MatKind kind, int ctas, cudaStream_t st) {
+constexpr size_t kMaxKtime = 1024;  // timed launches per job with in-kernel timestamps
+constexpr size_t kTicketSlots = kMaxStreams + 2;  // transfer streams, kernel stream, comm stream
+
+// Units are handed out dynamically (tickets) unless SLLM_STATIC_UNITS is set (A/B knob).
+static bool dynamic_units() {
+  static const bool on = getenv("SLLM_STATIC_UNITS") == nullptr;
+  return on;
+}
+
+static void launch(PartJob& j, bool prof, const MatParams& mp0, MatKind kind, int ctas, cudaStream_t st) {
+  MatParams mp = mp0;
+  if (prof && j.d_ktime && j.kev.size() < kMaxKtime) mp.ktime = j.d_ktime + 4 * j.kev.size();
+  size_t slot = 0;
+  while (slot < j.ticket_base.size() && j.ticket_base[slot].first != st) ++slot;
+  if (slot == j.ticket_base.size() && slot < kTicketSlots) j.ticket_base.push_back({st, 0});
+  if (j.d_tickets && slot < j.ticket_base.size()) {
+    mp.ticket = j.d_tickets + slot;
+    mp.ticket_base = j.ticket_base[slot].second;
+  }
   auto e = timed_begin(prof, st);
-  SLLM_CUDA(launch_materialise(mp, kind, ctas, st));
+  uint64_t drawn = 0;
+  SLLM_CUDA(launch_materialise(mp, kind, ctas, st, &drawn));
+  if (mp.ticket) j.ticket_base[slot].second += drawn;
   timed_end(e, j.kev, st);
   if (prof) {
     j.kernel_bytes += mp.hi - mp.lo;
     j.kev_bytes.push_back(mp.hi - mp.lo);
   }
   j.launches++;
-}
-
-static void copy_h2d(PartJob& j, bool prof, void* dst, const void* src, uint64_t n, cudaStream_t st) {
-  auto e = timed_begin(prof, st);
-  SLLM_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
-  timed_end(e, j.cev, st);
-  j.copies++;
 }
 
 // Streams of one job: S transfer streams (copy engine or zero-copy kernels) and one
@@ -306,44 +324,24 @@ static MatParams window_params(const sllm_index& idx, const sllm_load_config& cf
 }
 
 // Copy chunks [k0, k1) (chunk k = partition bytes [k*C, min((k+1)*C, L))) from the pinned
-// source to dst + (k*C - lo) on stream xs: one cudaMemcpyBatchAsync for the whole window
-// when the runtime has it (one API call instead of k1-k0), else one cudaMemcpyAsync each.
+// source to dst + (k*C - lo) on stream xs.  The chunks of a window are contiguous on both
+// sides, so the window is ONE cudaMemcpyAsync of [k0*C, min(k1*C, L)): one host call per
+// >= 64 MiB instead of one per chunk (per-chunk calls at 1 MiB chunks made the host issue
+// loop the bottleneck: 41.8 GB/s, profiles/r01/sweep_opt67b.jsonl), and the copy engine
+// splits it into its own transfers.  (The batched-copy runtime entry point is not used:
+// it is closed on the B200 pool this build is measured on.)
 static void copy_window(PartJob& j, int prof, uint8_t* dst, const uint8_t* wsrc, uint64_t lo, uint64_t k0, uint64_t k1,
                         uint64_t C, uint64_t L, cudaStream_t xs) {
-  static std::atomic<int> batch_ok{1};
-  const uint64_t n = k1 - k0;
+  const uint64_t a = k0 * C, b = std::min(k1 * C, L);
+  if (b <= a) return;
   auto e = timed_begin(prof >= 2, xs);  // copies are timed only at profile level 2
-  if (n > 1 && batch_ok.load()) {
-    std::vector<void*> dsts(n), srcs(n);
-    std::vector<size_t> sizes(n);
-    for (uint64_t i = 0; i < n; ++i) {
-      const uint64_t a = (k0 + i) * C, b = std::min(a + C, L);
-      dsts[i] = dst + (a - lo);
-      srcs[i] = const_cast<uint8_t*>(wsrc + (a - lo));
-      sizes[i] = b - a;
-    }
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t zero = 0, fail_idx = 0;
-    cudaError_t r = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &zero, 1, &fail_idx, xs);
-    if (r == cudaSuccess) {
-      timed_end(e, j.cev, xs);
-      j.copies += 1;
-      return;
-    }
-    cudaGetLastError();
-    batch_ok = 0;  // not supported here: fall back for the rest of the process
-  }
-  for (uint64_t k = k0; k < k1; ++k) {
-    const uint64_t a = k * C, b = std::min(a + C, L);
-    SLLM_CUDA(cudaMemcpyAsync(dst + (a - lo), wsrc + (a - lo), b - a, cudaMemcpyHostToDevice, xs));
-    j.copies++;
-  }
+  SLLM_CUDA(cudaMemcpyAsync(dst + (a - lo), wsrc + (a - lo), b - a, cudaMemcpyHostToDevice, xs));
   timed_end(e, j.cev, xs);
+  j.copies++;
 }
 
 // Unit of the NCCL fan-outs' slicing and rounds: a whole copy window (>= kWindowBytes of
-// chunks), so every round is one batched copy submission and one grouped broadcast /
+// chunks), so every round is one copy submission and one grouped broadcast /
 // all-gather per root instead of one per chunk; the chunk stays the copy engine's
 // transfer unit inside it.  The P2P fan-out and unreplicated loads slice by chunk.
 uint64_t fanout_unit(uint64_t chunk, int32_t fanout) {
@@ -369,7 +367,7 @@ static uint64_t verify_tail_bytes(uint64_t L) {
 }
 
 // Issue the window of chunks [k0, k1) of job j: the copy engine moves every chunk (one
-// batched submission), then ONE verify / scatter launch covers the window; zero-copy
+// submission), then ONE verify / scatter launch covers the window; zero-copy
 // modes issue one kernel for the window.  Returns the stream whose completion means
 // "the window is in place and verified" (the fan-out orders its broadcast after it).
 static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, Pipe& P, uint64_t w,
@@ -568,7 +566,10 @@ static void run_job(sllm_load* L, PartJob& j) {
   // in ONE async copy from the set's pinned block, [block accumulators | computed
   // checksums] is zeroed by one memset -- two setup operations ahead of the first chunk.
   const size_t up_bytes = seg_bytes + gran_bytes + tab_bytes + 256;
-  const size_t zero_bytes = acc_bytes + tab_bytes;
+  static const bool ktime = getenv("SLLM_KTIME") != nullptr;
+  const size_t kt_bytes = (cfg.profile && ktime) ? kMaxKtime * 4 * sizeof(unsigned long long) : 0;
+  const size_t tk_bytes = dynamic_units() ? align_up(kTicketSlots * sizeof(unsigned long long), 256) : 0;
+  const size_t zero_bytes = acc_bytes + tab_bytes + kt_bytes + tk_bytes;
   const size_t total = up_bytes + zero_bytes;
   if (j.origin) SLLM_CUDA(cudaStreamWaitEvent(s0, j.ev[3], 0));  // recorded by sllm_load_start
   SLLM_CUDA(cudaMallocAsync(&j.scratch, total, s0));
@@ -592,6 +593,10 @@ static void run_job(sllm_load* L, PartJob& j) {
   j.d_err = reinterpret_cast<uint32_t*>(j.d_bad + 1);
   j.d_acc = reinterpret_cast<BlockAcc*>(base + up_bytes);
   j.d_cs = reinterpret_cast<uint64_t*>(base + up_bytes + acc_bytes);
+  j.d_ktime = kt_bytes ? reinterpret_cast<unsigned long long*>(base + up_bytes + acc_bytes + tab_bytes) : nullptr;
+  j.d_tickets = tk_bytes ? reinterpret_cast<unsigned long long*>(base + up_bytes + acc_bytes + tab_bytes + kt_bytes)
+                         : nullptr;
+  j.ticket_base.clear();
   SLLM_CUDA(cudaMemcpyAsync(base, h, up_bytes, cudaMemcpyHostToDevice, s0));
   SLLM_CUDA(cudaMemsetAsync(base + up_bytes, 0, zero_bytes, s0));
   SLLM_CUDA(cudaEventRecord(j.ev[0], s0));
@@ -783,6 +788,11 @@ static void run_job(sllm_load* L, PartJob& j) {
   j.h_err = (uint32_t)tail[1];
   SLLM_CUDA(cudaEventElapsedTime(&j.t_dev_ms, j.ev[0], j.ev[1]));
   static const bool dump = getenv("SLLM_PROFILE_DUMP") != nullptr;  // per-launch timeline on stderr
+  std::vector<unsigned long long> kt;
+  if (dump && j.d_ktime && !j.kev.empty()) {  // in-kernel timestamps (the job's work is complete)
+    kt.resize(4 * std::min(j.kev.size(), kMaxKtime));
+    SLLM_CUDA(cudaMemcpy(kt.data(), j.d_ktime, kt.size() * sizeof(kt[0]), cudaMemcpyDeviceToHost));
+  }
   for (auto* v : {&j.kev, &j.cev}) {
     double sum = 0;
     for (size_t i = 0; i < v->size(); ++i) {
@@ -793,10 +803,16 @@ static void run_job(sllm_load* L, PartJob& j) {
       if (dump) {
         float at = 0;
         SLLM_CUDA(cudaEventElapsedTime(&at, j.ev[0], e.first));
-        if (v == &j.kev)
-          fprintf(stderr, "sllm-prof p=%zu kernel=%zu start_ms=%.4f ms=%.4f bytes=%llu GBps=%.1f\n", j.p, i, at, ms,
+        if (v == &j.kev) {
+          fprintf(stderr, "sllm-prof p=%zu kernel=%zu start_ms=%.4f ms=%.4f bytes=%llu GBps=%.1f", j.p, i, at, ms,
                   (unsigned long long)j.kev_bytes[i], j.kev_bytes[i] / (ms * 1e6));
-        else
+          if (4 * i + 3 < kt.size()) {  // kernel span (first CTA start .. last CTA end), CTA start / end spread
+            const unsigned long long s0 = ~kt[4 * i], s1 = kt[4 * i + 1], e0 = ~kt[4 * i + 2], e1 = kt[4 * i + 3];
+            fprintf(stderr, " span_ms=%.4f start_spread_us=%.2f end_spread_us=%.2f", (e1 - s0) * 1e-6,
+                    (s1 - s0) * 1e-3, (e1 - e0) * 1e-3);
+          }
+          fprintf(stderr, "\n");
+        } else
           fprintf(stderr, "sllm-prof p=%zu copy=%zu start_ms=%.4f ms=%.4f\n", j.p, i, at, ms);
       }
       cudaEventDestroy(e.first);

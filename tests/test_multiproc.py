@@ -243,7 +243,7 @@ def test_allgather_round_errors():
 
 def test_fanout_unit():
     """The NCCL fan-outs slice and run rounds in whole >= 64 MiB windows of chunks (one
-    batched copy + one grouped collective per round); P2P / none keep the chunk.  The
+    copy + one grouped collective per round); P2P / none keep the chunk.  The
     schedule functions replayed above are the ones the loader calls with this unit."""
     import paper_2401_14351_b200 as sllm
     M = 1 << 20

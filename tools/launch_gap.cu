@@ -1,0 +1,80 @@
+// Where the time between a kernel's CUDA events and its own execution goes (diagnostic,
+// never the product): for a kernel shaped like the ring kernel (148 CTAs x 320 threads,
+// 196.8 KB dynamic shared memory) and for a plain one (0 B), launched alone between two
+// events, report the event-to-event time and the in-kernel span (first CTA start to last
+// CTA end, %globaltimer).  Their difference is launch + completion overhead.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o build/launch_gap tools/launch_gap.cu
+//   build/launch_gap [spin_us]
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+__device__ __forceinline__ unsigned long long gt() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// every CTA spins for spin_ns, then marks [~min start, max end]
+__global__ void spin_kernel(unsigned long long* kt, unsigned long long spin_ns) {
+  extern __shared__ unsigned char smem[];
+  const unsigned long long t0 = gt();
+  if (threadIdx.x == 0) atomicMax(kt, ~t0);
+  while (gt() - t0 < spin_ns) {
+  }
+  if (threadIdx.x == 0) smem[0] = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(kt + 1, gt());
+}
+
+#define CK(x)                                                                     \
+  do {                                                                            \
+    cudaError_t e_ = (x);                                                         \
+    if (e_ != cudaSuccess) {                                                      \
+      fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+      exit(1);                                                                    \
+    }                                                                             \
+  } while (0)
+
+int main(int argc, char** argv) {
+  const unsigned long long spin_us = argc > 1 ? atoll(argv[1]) : 300;
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int big = 12 * 16384 + 2 * 12 * 8;  // the ring kernel's dynamic shared memory
+  CK(cudaFuncSetAttribute(spin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+  unsigned long long* kt;
+  CK(cudaMalloc(&kt, 16));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (int smem : {0, big}) {
+    std::vector<double> ev_us, span_us;
+    for (int rep = 0; rep < 40; ++rep) {
+      CK(cudaMemsetAsync(kt, 0, 16, st));
+      CK(cudaEventRecord(a, st));
+      spin_kernel<<<sms, 320, smem, st>>>(kt, spin_us * 1000);
+      CK(cudaEventRecord(b, st));
+      CK(cudaStreamSynchronize(st));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      unsigned long long h[2];
+      CK(cudaMemcpy(h, kt, 16, cudaMemcpyDeviceToHost));
+      if (rep < 5) continue;  // warm-up
+      ev_us.push_back(ms * 1e3);
+      span_us.push_back((h[1] - ~h[0]) * 1e-3);
+    }
+    std::sort(ev_us.begin(), ev_us.end());
+    std::sort(span_us.begin(), span_us.end());
+    const size_t m = ev_us.size() / 2;
+    printf("{\"smem\": %d, \"spin_us\": %llu, \"event_us_median\": %.2f, \"span_us_median\": %.2f, "
+           "\"overhead_us_median\": %.2f, \"event_us_min\": %.2f}\n",
+           smem, spin_us, ev_us[m], span_us[m], ev_us[m] - span_us[m], ev_us[0]);
+  }
+  return 0;
+}

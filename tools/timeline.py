@@ -2,6 +2,9 @@
 kernel launch with its start (ms after the load's first event) and duration.
 
     SLLM_PROFILE_DUMP=1 python tools/timeline.py [--config lora-70b-r32] [--chunk-mib 64] [--streams 2]
+
+With SLLM_KTIME=1 every kernel line also carries the in-kernel span (first CTA start to last
+CTA end, %globaltimer) and the CTA start / end spreads, next to the CUDA-event duration.
 """
 import argparse
 import os
@@ -18,6 +21,7 @@ def main():
     ap.add_argument("--chunk-mib", type=int, default=64)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--profile", type=int, default=2, help="1: kernel launches timed, 2: copies too")
     args = ap.parse_args()
     import torch
     import paper_2401_14351_b200 as sllm
@@ -25,7 +29,7 @@ def main():
     from synth import models
     inv, seed = models.model_inventory(args.config)
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=[0], gpu_of={0: 0})
-    cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, n_streams=args.streams, mode=args.mode, profile=2)
+    cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, n_streams=args.streams, mode=args.mode, profile=args.profile)
     bases, per = sllm.allocate(idx, {0: 0}, cfg.scatter)
     for r in range(args.reps):
         print(f"--- load {r}", file=sys.stderr, flush=True)
