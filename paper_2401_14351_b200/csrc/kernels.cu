@@ -207,6 +207,7 @@ constexpr int kConsumerUnroll = SLLM_CONSUMER_UNROLL;
 constexpr uint32_t kStageBytes = SLLM_STAGE_KIB << 10;  // ring: kStages x kStageBytes = 192 KiB
 constexpr int kStages = (192 << 10) / kStageBytes;
 constexpr uint64_t kMaxUnitBytes = 1ull << 20;  // default: whole 1 MiB blocks when the launch is balanced
+constexpr uint32_t kFineTail = 4;  // fine-tail units per block (see launch_tma)
 constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + 2 * kStages * sizeof(uint64_t);
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -288,7 +289,31 @@ __device__ __forceinline__ void ktime_mark(unsigned long long* kt, int which) {
 }
 
 constexpr uint64_t kNoUnit = ~0ull;
-// The unit index the producer stored for a stage, read after that stage's full-barrier wait
+// Work items of a launch: n_coarse units of `unit` bytes (a 1/split-th of a checksum block),
+// then -- the fine tail -- the rest of [lo, hi) in units of unit / fine bytes, so that the
+// CTAs that finish their coarse units at different times share the last wave in small
+// pieces (the launch ends within ~one fine unit of its last CTA).  Item i -> bytes [a, e).
+struct Items {
+  uint64_t unit, fine_unit, u_first, n_coarse, v_first, n;
+  __device__ Items(const MatParams& p, uint64_t blk) {
+    unit = blk / p.split;
+    fine_unit = unit / p.fine;
+    u_first = p.lo / unit;
+    n_coarse = p.n_coarse;
+    v_first = (u_first + n_coarse) * p.fine;
+    n = n_coarse + ((p.hi + fine_unit - 1) / fine_unit - v_first);
+  }
+  // bytes of item i and the size of the piece it is of its checksum block
+  __device__ __forceinline__ void range(const MatParams& p, uint64_t i, uint64_t& a, uint64_t& e, uint64_t& sz) const {
+    const bool c = i < n_coarse;
+    sz = c ? unit : fine_unit;
+    const uint64_t k = c ? u_first + i : v_first + (i - n_coarse);
+    a = max(k * sz, p.lo);
+    e = min((k + 1) * sz, p.hi);
+  }
+};
+
+// The item index the producer stored for a stage, read after that stage's full-barrier wait
 // (acquire) -- volatile so the compiler cannot hoist it above the wait.
 __device__ __forceinline__ uint64_t unit_of(const uint64_t* s_unit, uint32_t stage) {
   return *static_cast<const volatile uint64_t*>(s_unit + stage);
@@ -304,14 +329,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   __shared__ unsigned long long s_red[2][3][kConsumerWarps];  // double-buffered by unit parity
-  __shared__ uint64_t s_unit[kStages];  // unit whose first stage is in the slot (kNoUnit: end)
+  __shared__ uint64_t s_unit[kStages];  // item whose first stage is in the slot (kNoUnit: end)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Work unit: a 1/split-th of a checksum block (a CTA owns whole units).  split > 1 lets
   // a launch covering few blocks still spread over every SM; the partial sums of a
   // block's units are then combined with atomics and finalised by its last unit.
   const uint64_t blk = kCheck ? p.block : (1ull << 20);
-  const uint64_t unit = blk / p.split;
-  const uint64_t u_first = p.lo / unit, u_end = (p.hi + unit - 1) / unit;
+  const Items items(p, blk);
   if (p.ktime && threadIdx.x == 0) ktime_mark(p.ktime, 0);
 
   // engine 2: the tensor bytes leave shared memory by TMA bulk stores issued by one
@@ -331,9 +355,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   if (warp == 0) {  // producer: picks the CTA's units and streams them through the ring
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      uint64_t u = u_first + blockIdx.x;  // first unit: static (grid <= units)
+      uint64_t u = blockIdx.x;  // first item: static (grid <= items)
       for (;;) {
-        const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
+        uint64_t a, e, sz;
+        items.range(p, u, a, e, sz);
         for (uint64_t off = a; off < e; off += kStageBytes) {
           const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
           mbar_wait(&empty[stage], phase ^ 1);
@@ -347,8 +372,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
         }
         // next unit: dynamic (a ticket, drawn once this unit is fully issued -- the ring
         // still holds up to 12 stages for the consumers, which hides the atomic) or static
-        u = p.ticket ? u_first + gridDim.x + (atomicAdd(p.ticket, 1ull) - p.ticket_base) : u + gridDim.x;
-        if (u >= u_end) break;
+        u = p.ticket ? gridDim.x + (atomicAdd(p.ticket, 1ull) - p.ticket_base) : u + gridDim.x;
+        if (u >= items.n) break;
       }
       mbar_wait(&empty[stage], phase ^ 1);
       s_unit[stage] = kNoUnit;  // end of the CTA's work: a stage with no bytes
@@ -366,7 +391,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
         mbar_wait(&full[stage], phase);
         const uint64_t u = unit_of(s_unit, stage);
         if (u == kNoUnit) break;
-        const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
+        uint64_t a, e, sz;
+        items.range(p, u, a, e, sz);
         uint32_t cur = find_seg(p, a);
         Seg sg = p.segs[cur];
         for (uint64_t off = a; off < e; off += kStageBytes) {
@@ -407,12 +433,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
     mbar_wait(&full[stage], phase);  // first stage of the CTA's next unit (or the end mark)
     const uint64_t u = unit_of(s_unit, stage);
     if (u == kNoUnit) break;
-    const uint64_t a = max(u * unit, p.lo), e = min((u + 1) * unit, p.hi);
+    uint64_t a, e, unit;  // unit: this item's piece size (coarse or fine)
+    items.range(p, u, a, e, unit);
     // segment holding byte a (same search in every thread: uniform, L1-cached)
     uint32_t cur = p.seg_begin;
     if (kStore) cur = find_seg(p, a);
     Seg sg = kStore ? p.segs[cur] : Seg{0, 0, nullptr, 0};
-    const uint64_t bstart = (u * unit / blk) * blk;  // first byte of this unit's checksum block
+    const uint64_t bstart = (a / blk) * blk;  // first byte of this item's checksum block
     unsigned long long A = 0, Bs = 0, Cs = 0;
     for (uint64_t off = a; off < e; off += kStageBytes) {
       const uint32_t n = (uint32_t)min((uint64_t)kStageBytes, e - off);
@@ -482,10 +509,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           SC += s_red[par][2][w];
         }
         unsigned long long fa = fold(SA), fb = fold(SB), fc = fold(SC);
-        const uint64_t j = u * unit / blk;
+        const uint64_t j = a / blk;
         const uint64_t blen = min(blk, p.part_len - j * blk);
         bool last = true;
-        if (p.split > 1) {  // combine this unit's partial sums with the block's other units
+        if (unit < blk) {  // combine this piece's partial sums with the block's other pieces
           BlockAcc* acc = p.acc + j;
           atomicAdd(&acc->a, fa);
           atomicAdd(&acc->b, fb);
@@ -602,18 +629,32 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream,
   MatParams q = p;
   const uint64_t blk = kCheck ? p.block : (1ull << 20);
   const int sms = num_sms();
+  const uint64_t G = (uint64_t)(grid < 1 ? sms : grid);
   q.split = 1;
   const uint64_t blocks = (p.hi + blk - 1) / blk - p.lo / blk;
   auto can_halve = [&](uint32_t s) { return s < 16 && blk / (2 * s) >= kStageBytes && (blk / (2 * s)) % 16 == 0; };
   while (can_halve(q.split) && blocks * q.split < 2ull * sms) q.split *= 2;
-  // Wave balance: a launch of U equal units on G CTAs takes ceil(U/G) unit-times, so keep
-  // halving the unit (down to 64 KiB) until U / (ceil(U/G) * G) >= 0.95 -- e.g. a 397-block
-  // verification span on 148 SMs runs 2.68 of 3 waves (89 %) at split 1, 97.5 % at split 4.
+  // Fine tail (SLLM_FINE_TAIL=0 turns it off: A/B knob): a launch of >= 2 waves of whole
+  // blocks hands out its last wave (G blocks) in quarter blocks, so CTAs that finish their
+  // whole blocks at different times (dynamic distribution: up to one block-time apart)
+  // share the end in small pieces.  Measured end spread of a 4 GiB K4 with whole blocks:
+  // 22 us (one 1 MiB block at ~47 GB/s per SM).
+  static const bool fine_on = [] {
+    const char* e = getenv("SLLM_FINE_TAIL");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool tail = fine_on && q.split == 1 && blocks >= 2 * G && blk / kFineTail >= (64u << 10) &&
+                    (blk / kFineTail) % kStageBytes == 0;
+  // Wave balance (launches without the fine tail): a launch of U equal units on G CTAs
+  // takes ceil(U/G) unit-times, so keep halving the unit (down to 64 KiB) until
+  // U / (ceil(U/G) * G) >= 0.95 -- e.g. a 397-block span on 148 SMs runs 2.68 of 3 waves
+  // (89 %) at split 1, 97.5 % at split 4.
   auto balance = [&](uint32_t s) {
-    const uint64_t U = blocks * s, G = (uint64_t)(grid < 1 ? sms : grid);
+    const uint64_t U = blocks * s;
     return (double)U / (double)(((U + G - 1) / G) * G);
   };
-  while (can_halve(q.split) && blk / (2 * q.split) >= (64u << 10) && balance(q.split) < 0.95) q.split *= 2;
+  if (!tail)
+    while (can_halve(q.split) && blk / (2 * q.split) >= (64u << 10) && balance(q.split) < 0.95) q.split *= 2;
   // Largest unit (measurement knob SLLM_UNIT_KIB): smaller units shorten the launch's tail
   // (the last CTA to finish is at most one unit behind) at 4 atomics per unit.
   static const uint64_t max_unit = [] {
@@ -624,8 +665,16 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream,
   if (!kCheck) q.split = 1;
   const uint64_t unit = blk / q.split;
   const uint64_t units = (p.hi + unit - 1) / unit - p.lo / unit;
-  if ((uint64_t)grid > units) grid = (int)units;
-  if (tickets) *tickets = q.ticket ? units : 0;  // each CTA draws one ticket past the end
+  q.fine = 1;
+  q.n_coarse = units;
+  if (tail && q.split == 1) {
+    q.fine = kFineTail;
+    q.n_coarse = units - G;
+  }
+  const uint64_t fine_unit = unit / q.fine;
+  const uint64_t n_items = q.n_coarse + ((p.hi + fine_unit - 1) / fine_unit - (p.lo / unit + q.n_coarse) * q.fine);
+  if ((uint64_t)grid > n_items) grid = (int)n_items;
+  if (tickets) *tickets = q.ticket ? n_items : 0;  // each CTA draws one ticket past the end
   materialise_tma_kernel<kStore, kCheck, kMc><<<grid, kTmaThreads, kTmaSmem, stream>>>(q);
   return cudaGetLastError();
 }

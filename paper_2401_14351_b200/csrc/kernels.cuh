@@ -49,6 +49,10 @@ struct MatParams {
   int engine;                // 0: LDG/STG tiles; 1: TMA bulk loads through a shared-memory ring,
                              // STG stores; 2: as 1 with TMA bulk stores out of the ring
   uint32_t split;            // TMA engine: units per checksum block (set by the launcher)
+  // TMA engine fine tail (set by the launcher): the first n_coarse units are whole units,
+  // the rest of the range is cut into units of unit / fine bytes (fine = 1: no tail)
+  uint32_t fine;
+  uint64_t n_coarse;
   // P2P fan-out (TMA engine, contiguous single segment): every stored vector of partition
   // offset x also goes to peer[k] + x -- device pointers to the other GPUs' replicas,
   // written over NVLink -- and, with no_seg_store, only there (CE: the source is the

@@ -20,13 +20,13 @@ __device__ __forceinline__ unsigned long long gt() {
 }
 
 // every CTA spins for spin_ns, then marks [~min start, max end]
-__global__ void spin_kernel(unsigned long long* kt, unsigned long long spin_ns) {
+__global__ void spin_kernel(unsigned long long* kt, unsigned long long spin_ns, int touch) {
   extern __shared__ unsigned char smem[];
   const unsigned long long t0 = gt();
   if (threadIdx.x == 0) atomicMax(kt, ~t0);
   while (gt() - t0 < spin_ns) {
   }
-  if (threadIdx.x == 0) smem[0] = 1;
+  if (threadIdx.x == 0 && touch) smem[0] = 1;  // (only with dynamic shared memory)
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(kt + 1, gt());
 }
@@ -53,12 +53,29 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
-  for (int smem : {0, big}) {
+  // "after_copy": like the loader's kernel stream, st first waits for a 64 MiB host->device
+  // copy on another stream (the event pair brackets only the kernel, as in the pipeline)
+  cudaStream_t cs;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaEvent_t landed;
+  CK(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
+  const size_t cbytes = 64ull << 20;
+  void *hsrc, *ddst;
+  CK(cudaMallocHost(&hsrc, cbytes));
+  CK(cudaMalloc(&ddst, cbytes));
+  for (int variant = 0; variant < 3; ++variant) {
+    const int smem = variant == 0 ? 0 : big;
+    const bool after_copy = variant == 2;
     std::vector<double> ev_us, span_us;
     for (int rep = 0; rep < 40; ++rep) {
       CK(cudaMemsetAsync(kt, 0, 16, st));
+      if (after_copy) {
+        CK(cudaMemcpyAsync(ddst, hsrc, cbytes, cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(landed, cs));
+        CK(cudaStreamWaitEvent(st, landed, 0));
+      }
       CK(cudaEventRecord(a, st));
-      spin_kernel<<<sms, 320, smem, st>>>(kt, spin_us * 1000);
+      spin_kernel<<<sms, 320, smem, st>>>(kt, spin_us * 1000, smem > 0);
       CK(cudaEventRecord(b, st));
       CK(cudaStreamSynchronize(st));
       float ms;
@@ -72,9 +89,9 @@ int main(int argc, char** argv) {
     std::sort(ev_us.begin(), ev_us.end());
     std::sort(span_us.begin(), span_us.end());
     const size_t m = ev_us.size() / 2;
-    printf("{\"smem\": %d, \"spin_us\": %llu, \"event_us_median\": %.2f, \"span_us_median\": %.2f, "
+    printf("{\"smem\": %d, \"after_copy\": %d, \"spin_us\": %llu, \"event_us_median\": %.2f, \"span_us_median\": %.2f, "
            "\"overhead_us_median\": %.2f, \"event_us_min\": %.2f}\n",
-           smem, spin_us, ev_us[m], span_us[m], ev_us[m] - span_us[m], ev_us[0]);
+           smem, (int)after_copy, spin_us, ev_us[m], span_us[m], ev_us[m] - span_us[m], ev_us[0]);
   }
   return 0;
 }
