@@ -1,6 +1,7 @@
 // Device-resident entry points of the kernels (K4 checksum, K3 scatter) for partitions
 // already in HBM -- also how bench.py measures them standalone against the HBM roofline.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -58,7 +59,16 @@ void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint6
   mp.bad = bad;
   mp.engine = standalone_engine();
   if (!getenv("SLLM_STATIC_UNITS")) mp.ticket = ticket;  // dynamic unit distribution (base 0)
+  static const bool ktime = getenv("SLLM_KTIME") != nullptr;  // diagnostic: in-kernel span on stderr
+  if (ktime) mp.ktime = reinterpret_cast<unsigned long long*>(b + acc_bytes + 320);
   SLLM_CUDA(launch_materialise(mp, MatKind::kChecksumOnly, ctas > 0 ? ctas : default_grid(), st));
+  if (ktime) {
+    unsigned long long kt[4];
+    SLLM_CUDA(cudaMemcpyAsync(kt, mp.ktime, sizeof(kt), cudaMemcpyDeviceToHost, st));
+    SLLM_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "sllm-ktime bytes=%llu span_ms=%.4f end_spread_us=%.2f\n", (unsigned long long)len,
+            (kt[3] - ~kt[0]) * 1e-6, (kt[3] - ~kt[2]) * 1e-3);
+  }
   SLLM_CUDA(cudaFreeAsync(scratch, st));
 }
 

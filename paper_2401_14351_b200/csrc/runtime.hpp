@@ -43,6 +43,7 @@ struct NvtxRange {
 constexpr int kMaxStreams = 8;
 constexpr uint32_t kTile = 64u << 10;  // bytes per kernel work tile
 constexpr uint64_t kWindowBytes = 64ull << 20;   // min bytes per copy submission / kernel launch
+constexpr uint64_t kCopyWindowMaxBytes = 256ull << 20;  // max bytes per copy submission (large partitions)
 constexpr uint64_t kVerifyBytes = 4096ull << 20;  // CE mode: max bytes per verification launch
                                                   // (span sweep r02: 2 -> 4 GiB spans, K4 0.91 -> 0.94 of HBM, step unchanged)
 constexpr uint64_t kVerifyTailBytes = 512ull << 20;  // CE mode: min span once the load's end is near

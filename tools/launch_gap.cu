@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -59,13 +60,27 @@ int main(int argc, char** argv) {
   CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   cudaEvent_t landed;
   CK(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
-  const size_t cbytes = 64ull << 20;
+  const size_t cbytes = 64ull << 20, big_copy = 1ull << 30;
   void *hsrc, *ddst;
-  CK(cudaMallocHost(&hsrc, cbytes));
-  CK(cudaMalloc(&ddst, cbytes));
-  for (int variant = 0; variant < 3; ++variant) {
+  CK(cudaMallocHost(&hsrc, big_copy));
+  CK(cudaMalloc(&ddst, big_copy));
+  // variants: 0 plain (0 B smem), 1 ring-kernel smem, 2 after a 64 MiB copy on another
+  // stream (waited), 3 while a 1 GiB host->device copy saturates PCIe on another stream,
+  // 4 as 3 with (event, kernel, event) launched as one CUDA graph
+  cudaGraphExec_t gexec = nullptr;
+  for (int variant = 0; variant < 5; ++variant) {
     const int smem = variant == 0 ? 0 : big;
-    const bool after_copy = variant == 2;
+    const bool after_copy = variant == 2, during_copy = variant >= 3, graph = variant == 4;
+    if (graph && !gexec) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      CK(cudaEventRecordWithFlags(a, st, cudaEventRecordExternal));
+      spin_kernel<<<sms, 320, smem, st>>>(kt, spin_us * 1000, smem > 0);
+      CK(cudaEventRecordWithFlags(b, st, cudaEventRecordExternal));
+      CK(cudaStreamEndCapture(st, &g));
+      CK(cudaGraphInstantiate(&gexec, g, 0));
+      CK(cudaGraphUpload(gexec, st));
+    }
     std::vector<double> ev_us, span_us;
     for (int rep = 0; rep < 40; ++rep) {
       CK(cudaMemsetAsync(kt, 0, 16, st));
@@ -74,10 +89,22 @@ int main(int argc, char** argv) {
         CK(cudaEventRecord(landed, cs));
         CK(cudaStreamWaitEvent(st, landed, 0));
       }
-      CK(cudaEventRecord(a, st));
-      spin_kernel<<<sms, 320, smem, st>>>(kt, spin_us * 1000, smem > 0);
-      CK(cudaEventRecord(b, st));
+      if (during_copy) {  // the kernel starts ~2 ms into a ~19 ms copy
+        CK(cudaMemcpyAsync(ddst, hsrc, big_copy, cudaMemcpyHostToDevice, cs));
+        CK(cudaStreamSynchronize(st));
+        const auto t0 = std::chrono::steady_clock::now();
+        while (std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(2)) {
+        }
+      }
+      if (graph) {
+        CK(cudaGraphLaunch(gexec, st));
+      } else {
+        CK(cudaEventRecord(a, st));
+        spin_kernel<<<sms, 320, smem, st>>>(kt, spin_us * 1000, smem > 0);
+        CK(cudaEventRecord(b, st));
+      }
       CK(cudaStreamSynchronize(st));
+      CK(cudaStreamSynchronize(cs));
       float ms;
       CK(cudaEventElapsedTime(&ms, a, b));
       unsigned long long h[2];
@@ -89,9 +116,11 @@ int main(int argc, char** argv) {
     std::sort(ev_us.begin(), ev_us.end());
     std::sort(span_us.begin(), span_us.end());
     const size_t m = ev_us.size() / 2;
-    printf("{\"smem\": %d, \"after_copy\": %d, \"spin_us\": %llu, \"event_us_median\": %.2f, \"span_us_median\": %.2f, "
-           "\"overhead_us_median\": %.2f, \"event_us_min\": %.2f}\n",
-           smem, (int)after_copy, spin_us, ev_us[m], span_us[m], ev_us[m] - span_us[m], ev_us[0]);
+    printf("{\"smem\": %d, \"after_copy\": %d, \"during_copy\": %d, \"graph\": %d, \"spin_us\": %llu, "
+           "\"event_us_median\": %.2f, \"span_us_median\": %.2f, \"overhead_us_median\": %.2f, \"event_us_min\": %.2f, "
+           "\"event_us_max\": %.2f}\n",
+           smem, (int)after_copy, (int)during_copy, (int)graph, spin_us, ev_us[m], span_us[m], ev_us[m] - span_us[m],
+           ev_us[0], ev_us.back());
   }
   return 0;
 }
