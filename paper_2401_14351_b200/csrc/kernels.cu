@@ -33,13 +33,22 @@ __device__ __forceinline__ unsigned long long fold(unsigned long long x) {
   return x >= kM ? x - kM : x;
 }
 
+#ifndef SLLM_HOST_L2_PREFETCH
+#define SLLM_HOST_L2_PREFETCH 0
+#endif
+
 template <bool kHostSrc>
 __device__ __forceinline__ uint4 load16(const uint8_t* p) {
   uint4 r;
   if (kHostSrc) {
     // host-mapped pinned memory over PCIe: plain global load, no L1 allocation
+#if SLLM_HOST_L2_PREFETCH == 256  // A/B knob: ask the L2 for 256-byte fills of the host lines
+    asm("ld.global.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+#else
     asm("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
         : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+#endif
   } else {
     asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
         : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
