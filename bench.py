@@ -812,7 +812,8 @@ def main(argv=None):
         comm = sllm.Comm.from_process_group(gpu) if world > 1 else sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, gpu)
 
     def step(prof: bool):
-        c = sllm.LoadConfig(**{**cfg.__dict__, "profile": prof})
+        # profile 3: per-launch CUDA events + in-kernel spans (two %globaltimer atomics per CTA)
+        c = sllm.LoadConfig(**{**cfg.__dict__, "profile": 3 if prof else 0})
         ix = sllm.Index.from_bytes(blob)                  # a1: open + validate the index
         res = sllm.load_start(ix, bufs, gpus, c, bases, per_tensor, streams, comm)
         return res, ix
@@ -921,8 +922,15 @@ def main(argv=None):
                 ("checksum only" if args.mode == "ce" else "scatter+checksum"),
                 "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
                 "bytes_per_launch": per_launch_bytes,
-                "note": "one CTA per SM; each launch verifies a span of landed windows (up to 4 GiB, halving towards the end) "
-                        "(1 MiB blocks split into equal units for wave balance) beside the PCIe copies"}
+                "note": "one CTA per SM, units handed out by ticket; each launch verifies a span of landed windows "
+                        "(up to 4 GiB, shrinking towards the end) beside the PCIe copies"}
+        span_ms = sum(r.get("t_kernel_span_ms_sum", 0.0) for r in reports) / len(reports)
+        if span_ms > 0:  # the same launches timed from inside (first CTA start .. last CTA end)
+            ach_in = per_launch_bytes / (span_ms / kern_launches * 1e-3) / 1e9
+            roof["in_kernel"] = {"achieved": ach_in, "frac": ach_in / hbm, "avg_span_ms": span_ms / kern_launches,
+                                 "what": "%globaltimer span of each launch; the CUDA-event time also holds the launch "
+                                         "and completion, which cost ~30 us each while the copy engine saturates "
+                                         "PCIe (profiles/r02/launch_gap.jsonl)"}
     if args.mode in ("zerocopy", "scatter_zc") and kern_launches and kern_ms > 0:
         # zero-copy kernel: every byte it reads crosses PCIe -> bound by the host link.
         # Launches on the S streams overlap, so the kernel's rate is its bytes per step

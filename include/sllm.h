@@ -304,7 +304,9 @@ typedef struct {
   int32_t fanout;       /* sllm_fanout; BCAST/ALLGATHER/P2P require a comm and a 1-partition index */
   int32_t verify;       /* 1 = check every block's Fletcher-64 against the index            */
   int32_t ctas;         /* CTAs per kernel launch (0 = mode default)                        */
-  int32_t profile;      /* 1 = time every kernel launch with CUDA events, 2 = also copies    */
+  int32_t profile;      /* 1 = time every kernel launch with CUDA events, 2 = also copies,
+                           3 = as 1 plus in-kernel spans (%globaltimer: first CTA start .. last
+                           CTA end of each timed launch, 2 atomics per CTA)                  */
   int32_t engine;       /* kernel engine: 0 = default (TMA), 1 = TMA bulk-load ring + vector stores,
                            2 = LDG/STG register tiles, 3 = TMA bulk-load ring + TMA bulk stores */
   int32_t reserved;     /* must be 0                                                        */
@@ -329,6 +331,8 @@ typedef struct {
   uint64_t storage_bytes;      /* file tier: bytes read from the partition files            */
   uint64_t t_storage_wait_ns_max; /* file tier: longest time a partition's GPU worker waited for
                                      storage (0 = storage never the bottleneck)              */
+  double t_kernel_span_ms_sum; /* profile 3: summed in-kernel spans of the timed launches (the
+                                  CUDA-event times above also hold launch and completion)   */
 } sllm_load_report;
 
 /* Communicator for SLLM_FANOUT_BCAST and SLLM_FANOUT_ALLGATHER.  One process per GPU: rank 0 calls

@@ -54,7 +54,8 @@ class LoadReport(C.Structure):
                 ("t_total_ns", C.c_uint64), ("t_issue_ns_max", C.c_uint64), ("t_device_ms_max", C.c_double),
                 ("t_kernel_ms_sum", C.c_double), ("t_copy_ms_sum", C.c_double), ("kernel_bytes", C.c_uint64),
                 ("bad_partition", C.c_int32), ("mode", C.c_int32), ("bad_block", C.c_uint64),
-                ("storage_bytes", C.c_uint64), ("t_storage_wait_ns_max", C.c_uint64)]
+                ("storage_bytes", C.c_uint64), ("t_storage_wait_ns_max", C.c_uint64),
+                ("t_kernel_span_ms_sum", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

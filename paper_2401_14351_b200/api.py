@@ -395,7 +395,7 @@ class LoadConfig:
     fanout: str = "none"          # none | bcast / allgather (NCCL) | p2p (fused NVLink stores) | nvls (multicast)
     verify: bool = True
     ctas: int = 0
-    profile: bool = False         # per-launch CUDA-event timing (bench roofline)
+    profile: int = 0              # 1 per-launch CUDA events (bench roofline), 2 + copies, 3 + in-kernel spans
     engine: str = "tma"           # tma (bulk-load smem ring) | tma_store (+ bulk stores) | ldg (register tiles)
 
     def to_c(self) -> _abi.LoadConfig:

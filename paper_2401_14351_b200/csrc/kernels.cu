@@ -643,25 +643,26 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream,
   const uint64_t blocks = (p.hi + blk - 1) / blk - p.lo / blk;
   auto can_halve = [&](uint32_t s) { return s < 16 && blk / (2 * s) >= kStageBytes && (blk / (2 * s)) % 16 == 0; };
   while (can_halve(q.split) && blocks * q.split < 2ull * sms) q.split *= 2;
-  // Fine tail (SLLM_FINE_TAIL=0 turns it off: A/B knob): a launch of >= 2 waves of whole
-  // blocks hands out its last wave (G blocks) in quarter blocks, so CTAs that finish their
-  // whole blocks at different times (dynamic distribution: up to one block-time apart)
-  // share the end in small pieces.  Measured end spread of a 4 GiB K4 with whole blocks:
-  // 22 us (one 1 MiB block at ~47 GB/s per SM).
-  static const bool fine_on = [] {
-    const char* e = getenv("SLLM_FINE_TAIL");
-    return !(e && atoi(e) == 0);
-  }();
-  const bool tail = fine_on && q.split == 1 && blocks >= 2 * G && blk / kFineTail >= (64u << 10) &&
-                    (blk / kFineTail) % kStageBytes == 0;
-  // Wave balance (launches without the fine tail): a launch of U equal units on G CTAs
-  // takes ceil(U/G) unit-times, so keep halving the unit (down to 64 KiB) until
-  // U / (ceil(U/G) * G) >= 0.95 -- e.g. a 397-block span on 148 SMs runs 2.68 of 3 waves
-  // (89 %) at split 1, 97.5 % at split 4.
+  // Wave balance: a launch of U equal units on G CTAs runs ceil(U/G) waves, the last one
+  // U/G - floor(U/G) full -- e.g. a 397-block span on 148 SMs runs 2.68 of 3 waves (89 %).
   auto balance = [&](uint32_t s) {
     const uint64_t U = blocks * s;
     return (double)U / (double)(((U + G - 1) / G) * G);
   };
+  // Fine tail (SLLM_FINE_TAIL=0 turns it off: A/B knob): a launch of >= 2 waves of whole
+  // blocks whose last wave is < 95 % full hands out its last G blocks in quarter blocks
+  // instead of splitting every block, so only the end pays the per-piece combine.  In-kernel
+  // spans (profiles/r02/fine_tail/, r02v): 470 MB (448 blocks, 76 % last wave) 0.113 ms with
+  // every block in eighths vs 0.084 with the fine tail; balanced launches are faster without
+  // it (4 GiB: 0.6125 vs 0.6166 ms; 576 blocks: 0.093 vs 0.102 ms).
+  static const bool fine_on = [] {
+    const char* e = getenv("SLLM_FINE_TAIL");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool tail = fine_on && q.split == 1 && blocks >= 2 * G && balance(1) < 0.95 &&
+                    blk / kFineTail >= (64u << 10) && (blk / kFineTail) % kStageBytes == 0;
+  // Otherwise keep halving the unit (down to 64 KiB) until the last wave is >= 95 % full
+  // (the 397-block span: 97.5 % at split 4).
   if (!tail)
     while (can_halve(q.split) && blk / (2 * q.split) >= (64u << 10) && balance(q.split) < 0.95) q.split *= 2;
   // Largest unit (measurement knob SLLM_UNIT_KIB): smaller units shorten the launch's tail

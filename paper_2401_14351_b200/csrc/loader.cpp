@@ -131,7 +131,8 @@ struct PartJob {
   uint64_t* d_expect = nullptr;
   uint64_t* d_cs = nullptr;
   unsigned long long* d_bad = nullptr;
-  unsigned long long* d_ktime = nullptr;  // diagnostic (SLLM_KTIME + profile): MatParams.ktime slots
+  unsigned long long* d_ktime = nullptr;  // profile 3 / SLLM_KTIME: MatParams.ktime slots
+  unsigned long long* h_ktime = nullptr;  // their pinned copy (read back behind the load)
   // dynamic unit distribution (MatParams.ticket): one zeroed counter per launching stream,
   // with the tickets its earlier launches drew (launches on one stream run in order)
   unsigned long long* d_tickets = nullptr;
@@ -151,7 +152,7 @@ struct PartJob {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev, cev;
   std::vector<uint64_t> kev_bytes;  // bytes covered by each timed kernel launch
   uint64_t kernel_bytes = 0;
-  double kernel_ms = 0, copy_ms = 0;
+  double kernel_ms = 0, copy_ms = 0, kernel_span_ms = 0;
   std::thread th;
   std::vector<cudaStream_t> used;  // streams this job queued work on (drained on failure)
   StreamSet* ss = nullptr;         // leased from the GPU's DeviceCtx for the job's lifetime
@@ -575,7 +576,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   // checksums] is zeroed by one memset -- two setup operations ahead of the first chunk.
   const size_t up_bytes = seg_bytes + gran_bytes + tab_bytes + 256;
   static const bool ktime = getenv("SLLM_KTIME") != nullptr;
-  const size_t kt_bytes = (cfg.profile && ktime) ? kMaxKtime * 4 * sizeof(unsigned long long) : 0;
+  const size_t kt_bytes = (cfg.profile == 3 || (cfg.profile && ktime)) ? kMaxKtime * 4 * sizeof(unsigned long long) : 0;
   const size_t tk_bytes = dynamic_units() ? align_up(kTicketSlots * sizeof(unsigned long long), 256) : 0;
   const size_t zero_bytes = acc_bytes + tab_bytes + kt_bytes + tk_bytes;
   const size_t total = up_bytes + zero_bytes;
@@ -586,7 +587,7 @@ static void run_job(sllm_load* L, PartJob& j) {
     SLLM_CUDA(cudaMallocAsync(&st, (size_t)P.nslot * P.slot_bytes, s0));
     j.staging = static_cast<uint8_t*>(st);
   }
-  uint8_t* h = j.ss->host_stage(up_bytes + 256);
+  uint8_t* h = j.ss->host_stage(up_bytes + 256 + kt_bytes);
   j.h_result = h + up_bytes;  // 16 bytes: first failing block, peer-wait result
   std::memcpy(h, j.segs.data(), j.segs.size() * sizeof(Seg));
   if (!j.gran_seg.empty()) std::memcpy(h + seg_bytes, j.gran_seg.data(), j.gran_seg.size() * 4);
@@ -602,6 +603,7 @@ static void run_job(sllm_load* L, PartJob& j) {
   j.d_acc = reinterpret_cast<BlockAcc*>(base + up_bytes);
   j.d_cs = reinterpret_cast<uint64_t*>(base + up_bytes + acc_bytes);
   j.d_ktime = kt_bytes ? reinterpret_cast<unsigned long long*>(base + up_bytes + acc_bytes + tab_bytes) : nullptr;
+  j.h_ktime = kt_bytes ? reinterpret_cast<unsigned long long*>(h + up_bytes + 256) : nullptr;
   j.d_tickets = tk_bytes ? reinterpret_cast<unsigned long long*>(base + up_bytes + acc_bytes + tab_bytes + kt_bytes)
                          : nullptr;
   j.ticket_base.clear();
@@ -770,6 +772,9 @@ static void run_job(sllm_load* L, PartJob& j) {
   SLLM_CUDA(cudaEventRecord(j.ev[1], s0));
   // the result word comes back into the pinned block behind the load (no extra round trip)
   SLLM_CUDA(cudaMemcpyAsync(j.h_result, j.d_bad, 16, cudaMemcpyDeviceToHost, s0));
+  if (j.d_ktime && !j.kev.empty())  // profile 3: the timed launches' in-kernel stamps
+    SLLM_CUDA(cudaMemcpyAsync(j.h_ktime, j.d_ktime, 4 * sizeof(unsigned long long) * std::min(j.kev.size(), kMaxKtime),
+                              cudaMemcpyDeviceToHost, s0));
   {  // every command of this job is enqueued: the caller's stream may now wait on ev[1]
     std::lock_guard<std::mutex> g(L->issue_mu);
     j.issue_ok = j.issue_signalled = true;
@@ -797,9 +802,11 @@ static void run_job(sllm_load* L, PartJob& j) {
   SLLM_CUDA(cudaEventElapsedTime(&j.t_dev_ms, j.ev[0], j.ev[1]));
   static const bool dump = getenv("SLLM_PROFILE_DUMP") != nullptr;  // per-launch timeline on stderr
   std::vector<unsigned long long> kt;
-  if (dump && j.d_ktime && !j.kev.empty()) {  // in-kernel timestamps (the job's work is complete)
-    kt.resize(4 * std::min(j.kev.size(), kMaxKtime));
-    SLLM_CUDA(cudaMemcpy(kt.data(), j.d_ktime, kt.size() * sizeof(kt[0]), cudaMemcpyDeviceToHost));
+  j.kernel_span_ms = 0;
+  if (j.d_ktime && !j.kev.empty()) {  // in-kernel timestamps (the job's work is complete)
+    kt.assign(j.h_ktime, j.h_ktime + 4 * std::min(j.kev.size(), kMaxKtime));
+    for (size_t i = 0; i + 3 < kt.size(); i += 4)
+      if (kt[i + 3]) j.kernel_span_ms += (kt[i + 3] - ~kt[i]) * 1e-6;  // (a launch with no bytes has no marks)
   }
   for (auto* v : {&j.kev, &j.cev}) {
     double sum = 0;
@@ -896,7 +903,7 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   // loads (measured crossover).  Resolved below once the jobs are known.
   const bool auto_mode = cfg.mode == SLLM_MODE_AUTO;
   if (auto_mode) cfg.mode = SLLM_MODE_CE;
-  if (cfg.profile < 0 || cfg.profile > 2) fail(SLLM_E_INVALID, "profile must be 0, 1 or 2");
+  if (cfg.profile < 0 || cfg.profile > 3) fail(SLLM_E_INVALID, "profile must be 0, 1, 2 or 3");
   if (cfg.engine < 0 || cfg.engine > 3) fail(SLLM_E_INVALID, "unknown kernel engine");
   if (cfg.reserved) fail(SLLM_E_INVALID, "reserved config field must be 0");
   if (cfg.chunk_bytes % tile_for(*idx)) fail(SLLM_E_INVALID, "chunk size must be a multiple of the 64 KiB work tile");
@@ -1101,6 +1108,7 @@ static void join_load(sllm_load* L) {
     r.t_issue_ns_max = std::max(r.t_issue_ns_max, j.t_issue_ns);
     r.t_device_ms_max = std::max(r.t_device_ms_max, (double)j.t_dev_ms);
     r.t_kernel_ms_sum += j.kernel_ms;
+    r.t_kernel_span_ms_sum += j.kernel_span_ms;
     r.t_copy_ms_sum += j.copy_ms;
     r.kernel_bytes += j.kernel_bytes;
     r.storage_bytes += j.storage_bytes;
