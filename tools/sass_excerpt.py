@@ -11,7 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "paper_2401_14351_b200", "libsllm.so")
-KEEP = re.compile(r"^(UBLKCP|SYNCS|LDS\.128|SHFL\.BFLY|STG\.E|LDG\.E|ATOMG|RED\.|MEMBAR|NANOSLEEP|CS2R)")
+KEEP = re.compile(r"^(UBLKCP|SYNCS|LDS\.128|SHFL\.BFLY|STG\.E|LDG\.E|ATOMG|REDG|MEMBAR|NANOSLEEP|CS2R)")
 
 HEADER = """# cuobjdump -sass paper_2401_14351_b200/libsllm.so (sm_100a cubin), tools/sass_excerpt.py
 # per kernel: count of the Blackwell-native tile-movement / sync instructions
@@ -22,7 +22,7 @@ HEADER = """# cuobjdump -sass paper_2401_14351_b200/libsllm.so (sm_100a cubin), 
 #   STG.E.NA.128 = 16-byte stores (st.global.L1::no_allocate) into tensors / peer replicas
 #   STG.E.128   = the NVLS multicast store (multimem.st.global.v4.f32 on the multicast mapping)
 #   ATOMG.E.ADD.64 = ticket draws (dynamic units), split-block combines; ATOMG.E.MIN = failing block;
-#   RED.E.MAX.64 = profile-3 in-kernel span marks
+#   REDG.E.MAX.64 = profile-3 in-kernel span marks
 #   CS2R ... SR_GLOBALTIMERLO = %globaltimer (mbarrier watchdog, profile-3 in-kernel spans)
 """
 
