@@ -156,7 +156,8 @@ def max_over_ranks(x, world: int):
 
 
 def step_stats(ms):
-    return {"median": statistics.median(ms), "min": min(ms), "max": max(ms), "n": len(ms)}
+    return {"median": statistics.median(ms), "min": min(ms), "max": max(ms), "n": len(ms),
+            "all": [round(float(x), 3) for x in ms]}
 
 
 class ClockSampler:
@@ -819,7 +820,7 @@ def main(argv=None):
         return res, ix
 
     for _ in range(args.warmup):
-        res, ix = step(False)
+        res, ix = step(not args.no_profile)  # the timed steps' exact work (profile level included)
         res.wait()
         del res, ix
     if world > 1:

@@ -63,9 +63,33 @@ __device__ __forceinline__ void mc_store16(uint8_t* p, const uint4& v) {
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
+// L2 evict-first hints (profiles/r02/l2_hints/, ncu + bench A/B on one box): on the ring's
+// TMA bulk loads of the store kernels (K3 / K2 / fan-out) the read bytes leave L2 first and
+// the stores keep it -- K3 4.26 -> 4.19 ms per 26.6 GB, in-pipeline K3 0.899 -> 0.907
+// in-kernel; on K4 (read only) the hint costs ~1 % (0.622 -> 0.627 ms per 4 GiB), and on the
+// stores it costs 3 % (K3 4.39 ms), on host-mapped sources (K2) 1 %.  SLLM_LD_HINT: 0 never,
+// 1 every ring kernel, 2 (default) store kernels reading HBM only; SLLM_ST_HINT=1 puts the hint
+// on the stores (A/B knobs).
+#ifndef SLLM_ST_HINT
+#define SLLM_ST_HINT 0
+#endif
+#ifndef SLLM_LD_HINT
+#define SLLM_LD_HINT 2
+#endif
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ void store16(uint8_t* p, const uint4& v) {
+#if SLLM_ST_HINT
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(evict_first_policy()) : "memory");
+#else
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+#endif
 }
 
 // Store the first n (< 16) bytes of v at p (tensor tail; the rest of the vector is padding).
@@ -249,9 +273,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     }
   }
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, bool hint) {
+  if (hint) {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(evict_first_policy()) : "memory");
+  } else {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+  }
 }
 // smem -> global bulk copy (TMA store, SASS UBLKCP), tracked by bulk async-groups.
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
@@ -362,6 +391,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
   __syncthreads();
 
   if (warp == 0) {  // producer: picks the CTA's units and streams them through the ring
+    // L2 evict-first on the ring loads of the HBM-source store kernels (K3, CE fan-out); not on
+    // K4 (read only) nor on host-mapped sources (K2: 1 % slower with it, profiles/r02/l2_hints/)
+    const bool ld_hint = SLLM_LD_HINT == 1 || (SLLM_LD_HINT == 2 && kStore && !p.host_src);
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       uint64_t u = blockIdx.x;  // first item: static (grid <= items)
@@ -376,7 +408,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const M
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (off == a) s_unit[stage] = u;  // published by the arrive below (release)
           mbar_expect_tx(&full[stage], n);
-          bulk_g2s(smem + (size_t)stage * kStageBytes, p.src + (off - p.src_origin), n, &full[stage]);
+          bulk_g2s(smem + (size_t)stage * kStageBytes, p.src + (off - p.src_origin), n, &full[stage], ld_hint);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         // next unit: dynamic (a ticket, drawn once this unit is fully issued -- the ring
