@@ -23,9 +23,13 @@ namespace sllm {
 struct NvtxRange {
   template <class... A>
   explicit NvtxRange(const char* fmt, A... a) {
-    char b[96];
-    snprintf(b, sizeof b, fmt, a...);
-    nvtxRangePushA(b);
+    if constexpr (sizeof...(A) == 0) {
+      nvtxRangePushA(fmt);
+    } else {
+      char b[96];
+      snprintf(b, sizeof b, fmt, a...);
+      nvtxRangePushA(b);
+    }
   }
   ~NvtxRange() { nvtxRangePop(); }
   NvtxRange(const NvtxRange&) = delete;
