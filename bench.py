@@ -447,7 +447,7 @@ def choose_partitions(args, rank, world, n_parts, replicated):
 # ---------------------------------------------------------------------------------------
 # Rooflines measured in the same run
 # ---------------------------------------------------------------------------------------
-def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1, gpus=None):
+def h2d_peak(bufs, bases, torch, gib=4, reps=5, world=1, gpus=None):
     """B_h2d(N): the copy engine's best host->device rate from the same pinned buffer into
     the same destination over >= 4 GiB: max of one 4 GiB
     cudaMemcpyAsync and back-to-back 64 MiB cudaMemcpyAsync calls on one stream, best of
@@ -475,6 +475,10 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=3, world=1, gpus=None):
                 src, dst = bufs[p].torch()[:n], bases[p][:n]
                 with torch.cuda.device(g):
                     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    # hold the stream ~1 ms so every copy is enqueued before the start event
+                    # runs: the events then time the copy engine, not the host's copy issue
+                    # (which dominated the 13.6 MB toy copy: 18-25 "GB/s")
+                    torch.cuda._sleep(2_000_000)
                     s.record()
                     for o in range(0, n, piece or n):
                         dst[o:o + (piece or n)].copy_(src[o:o + (piece or n)], non_blocking=True)
