@@ -376,7 +376,7 @@ static uint64_t verify_tail_bytes(uint64_t L) {
 // "the window is in place and verified" (the fan-out orders its broadcast after it).
 static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, Pipe& P, uint64_t w,
                                  uint64_t k0, uint64_t k1, bool last) {
-  NvtxRange nv("sllm/window p=%zu w=%llu chunks=[%llu,%llu)", j.p, (unsigned long long)w, (unsigned long long)k0,
+  NvtxRange nv("sllm.window p=%zu w=%llu chunks=[%llu,%llu)", j.p, (unsigned long long)w, (unsigned long long)k0,
                (unsigned long long)k1);
   const bool check = cfg.verify && idx.block;
   const int prof = cfg.profile;
@@ -417,7 +417,7 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
         P.v_k1 = k1;
         const uint64_t pending = std::min(P.v_k1 * C, L) - P.v_k0 * C;
         if (last || pending >= verify_span_bytes() || (pending >= verify_tail_bytes(L) && pending >= L - hi)) {
-          NvtxRange nvv("sllm/verify/span [%llu,%llu)", (unsigned long long)(P.v_k0 * C),
+          NvtxRange nvv("sllm.verify.span [%llu,%llu)", (unsigned long long)(P.v_k0 * C),
                         (unsigned long long)std::min(P.v_k1 * C, L));
           MatParams vp = window_params(idx, cfg, j, P.v_k0, P.v_k1, P.v_k0 * C, std::min(P.v_k1 * C, L));
           vp.src = j.dst_base;
@@ -464,7 +464,7 @@ static cudaStream_t issue_window(const sllm_index& idx, const sllm_load_config& 
 // Checksum-only verification of bytes that arrived through the fan-out.
 static void verify_range(const sllm_index& idx, const sllm_load_config& cfg, PartJob& j, uint64_t lo, uint64_t hi,
                          cudaStream_t st) {
-  NvtxRange nv("sllm/verify/range [%llu,%llu)", (unsigned long long)lo, (unsigned long long)hi);
+  NvtxRange nv("sllm.verify.range [%llu,%llu)", (unsigned long long)lo, (unsigned long long)hi);
   MatParams mp{};
   mp.src = j.dst_base;
   mp.lo = lo;
@@ -495,7 +495,7 @@ static void join_streams(const std::vector<cudaStream_t>& tails, cudaStream_t s0
 }
 
 static void run_job(sllm_load* L, PartJob& j) {
-  NvtxRange nv("sllm/partition p=%zu gpu=%d", j.p, j.gpu);
+  NvtxRange nv("sllm.partition p=%zu gpu=%d", j.p, j.gpu);
   const sllm_index& idx = *L->idx;
   const sllm_load_config& cfg = L->cfg;
   const PartRec& pr = idx.parts[j.p];
@@ -676,7 +676,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       }
     };
     for (uint64_t r = 0; r < rounds; ++r) {
-      NvtxRange nvr("sllm/fanout/round %llu", (unsigned long long)r);
+      NvtxRange nvr("sllm.fanout.round %llu", (unsigned long long)r);
       full = 0;
       if (schedule(r, nullptr) != SLLM_OK) fail(SLLM_E_INVALID, "fan-out schedule failed");
       std::vector<std::pair<uint64_t, uint64_t>> ranges(R);
@@ -745,7 +745,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       for (uint64_t w = 0; w < P.plan.size(); ++w)
         issue_window(idx, cfg, j, P, w, P.plan[w].first, P.plan[w].second, w + 1 == P.plan.size());
     } else if (cfg.mode == SLLM_MODE_GDS) {
-      NvtxRange nvg("sllm/gds p=%zu", j.p);
+      NvtxRange nvg("sllm.gds p=%zu", j.p);
       // storage -> HBM with cuFile (gds.cpp); the landed prefix is verified in K4 spans on
       // the kernel stream with the CE pipeline's span rule
       SLLM_CUDA(cudaStreamSynchronize(s0));  // scratch and tables are in place before K4 runs
@@ -928,7 +928,7 @@ using namespace sllm;
 sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_config* cfg_in, const void* const* host_src,
                                      const int32_t* gpu, void* const* dst_base, void* const* dst_tensor,
                                      void* const* stream, sllm_comm* comm, const char* dir, int32_t io_threads) {
-  NvtxRange nv("sllm/load_start");
+  NvtxRange nv("sllm.load_start");
   if (!idx) fail(SLLM_E_INVALID, "null index");
   if (!idx->sealed) fail(SLLM_E_INVALID, "index is planned but not sealed");
   sllm_load_config cfg{};
@@ -1189,7 +1189,7 @@ static void join_load(sllm_load* L) {
 }
 
 sllm_status sllm_load_wait_internal(sllm_load* L, sllm_load_report* rep) {
-  NvtxRange nv("sllm/load_wait");
+  NvtxRange nv("sllm.load_wait");
   join_load(L);
   if (rep) *rep = L->rep;
   if (L->result != SLLM_OK) {

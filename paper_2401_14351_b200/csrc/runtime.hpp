@@ -17,9 +17,10 @@
 
 namespace sllm {
 
-// Host-side NVTX range around a load phase (SURVEY §5 tracing): "sllm/<phase> ...".  Free
-// unless a tool (ncu --nvtx, nsys) injects NVTX; lets ncu select e.g. only the verification
-// launches with --nvtx-include "sllm/verify/".
+// Host-side NVTX range around a load phase (SURVEY §5 tracing): "sllm.<phase> ...".  Free
+// unless a tool (ncu --nvtx, nsys) injects NVTX; ncu selects e.g. only the verification
+// launches with --nvtx --nvtx-include "regex:sllm\.verify\..*/" ('/' is ncu's range-nesting
+// separator, so the names use '.').
 struct NvtxRange {
   template <class... A>
   explicit NvtxRange(const char* fmt, A... a) {
