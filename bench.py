@@ -451,11 +451,18 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=5, world=1, gpus=None):
     """B_h2d(N): the copy engine's best host->device rate from the same pinned buffer into
     the same destination over >= 4 GiB: max of one 4 GiB
     cudaMemcpyAsync and back-to-back 64 MiB cudaMemcpyAsync calls on one stream, best of
-    `reps` each.  Under torchrun every rep starts on a barrier so all N links (and the host
+    `reps` each (plain cudaMemcpyAsync through the cuda-python runtime bindings when present,
+    queued behind a ~1 ms stream hold).  Under torchrun every rep starts on a barrier so all N links (and the host
     DRAM / PCIe switches they share) are loaded at once; the aggregate is N * bytes / the
     slowest rank's time.  With partitions on several GPUs of this process (--spread) one
     partition per GPU copies at once, aggregate = their bytes / the slowest GPU's time.
     Returns (aggregate GB/s, {method: aggregate GB/s})."""
+    try:  # the CUDA runtime bindings (cuda-python): copies issued without torch's copy_ path
+        from cuda.bindings import runtime as rt
+    except ImportError:
+        rt = None
+    if os.environ.get("SLLM_BENCH_PEAK_TORCH") == "1":  # A/B: torch copy_ instead
+        rt = None
     firsts = {}
     for p in sorted(bufs):
         firsts.setdefault(gpus[p] if gpus else torch.cuda.current_device(), p)
@@ -472,21 +479,40 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=5, world=1, gpus=None):
             evs = []
             for g, p in firsts.items():
                 n = sizes[g]
-                src, dst = bufs[p].torch()[:n], bases[p][:n]
+                step = piece or n
                 with torch.cuda.device(g):
-                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     # hold the stream ~1 ms so every copy is enqueued before the start event
                     # runs: the events then time the copy engine, not the host's copy issue
-                    # (which dominated the 13.6 MB toy copy: 18-25 "GB/s")
                     torch.cuda._sleep(2_000_000)
-                    s.record()
-                    for o in range(0, n, piece or n):
-                        dst[o:o + (piece or n)].copy_(src[o:o + (piece or n)], non_blocking=True)
-                    e.record()
+                    if rt is not None:  # plain cudaMemcpyAsync calls, no framework in the way
+                        st = torch.cuda.current_stream(g).cuda_stream
+                        rt.cudaSetDevice(g)
+                        s, e = rt.cudaEventCreate()[1], rt.cudaEventCreate()[1]
+                        rt.cudaEventRecord(s, st)
+                        for o in range(0, n, step):
+                            rt.cudaMemcpyAsync(bases[p].data_ptr() + o, bufs[p].ptr + o, min(step, n - o),
+                                               rt.cudaMemcpyKind.cudaMemcpyHostToDevice, st)
+                        rt.cudaEventRecord(e, st)
+                    else:
+                        src, dst = bufs[p].torch()[:n], bases[p][:n]
+                        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        s.record()
+                        for o in range(0, n, step):
+                            dst[o:o + step].copy_(src[o:o + step], non_blocking=True)
+                        e.record()
                 evs.append((s, e))
-            for s, e in evs:
-                e.synchronize()
-            ms = max_over_ranks(max(s.elapsed_time(e) for s, e in evs), world)
+            if rt is not None:
+                for s, e in evs:
+                    rt.cudaEventSynchronize(e)
+                times = [rt.cudaEventElapsedTime(s, e)[1] for s, e in evs]
+                for s, e in evs:
+                    rt.cudaEventDestroy(s)
+                    rt.cudaEventDestroy(e)
+            else:
+                for s, e in evs:
+                    e.synchronize()
+                times = [s.elapsed_time(e) for s, e in evs]
+            ms = max_over_ranks(max(times), world)
             best = max(best, world * sum(sizes.values()) / (ms * 1e-3) / 1e9)
         out[name] = best
     return max(out.values()), out
