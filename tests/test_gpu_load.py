@@ -122,6 +122,32 @@ def test_fault_injection_names_block(mode, engine):
         host[:] = clean
 
 
+def test_profile_levels():
+    """profile 1 times every kernel launch with CUDA events; 3 adds the launches' in-kernel
+    spans (first CTA start .. last CTA end), which lie inside the event times; 4 is rejected.
+    Profiling never changes the loaded bytes."""
+    inv, seed = models.model_inventory("toy")
+    idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+    lay, oparts, payloads = oracle_of(inv, seed, 4096, 1 << 20)
+    for mode in MODES:
+        for prof in (0, 1, 3):
+            cfg = sllm.LoadConfig(chunk_bytes=1 << 20, mode=mode, profile=prof)
+            res = sllm.load(idx, bufs, {0: 0}, cfg)
+            rep = res.report
+            check_against_oracle(res, idx, inv, lay, oparts, payloads, [0], cfg)
+            if prof == 0:
+                assert rep["t_kernel_ms_sum"] == 0 and rep["t_kernel_span_ms_sum"] == 0
+            else:
+                assert rep["t_kernel_ms_sum"] > 0 and rep["kernel_bytes"] > 0, (mode, prof)
+            if prof == 3:
+                assert 0 < rep["t_kernel_span_ms_sum"] <= rep["t_kernel_ms_sum"], (mode, rep)
+            elif prof == 1:
+                assert rep["t_kernel_span_ms_sum"] == 0
+    with pytest.raises(sllm.SllmError) as ex:
+        sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, profile=4))
+    assert ex.value.status == 1
+
+
 def test_verify_off_still_exact():
     inv, seed = models.model_inventory("toy")
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
