@@ -447,6 +447,14 @@ def choose_partitions(args, rank, world, n_parts, replicated):
 # ---------------------------------------------------------------------------------------
 # Rooflines measured in the same run
 # ---------------------------------------------------------------------------------------
+def _rt_ok(rt, ret):
+    """Unwrap a cuda-python runtime call's (error, value...) tuple; raise on any error."""
+    ret = ret if isinstance(ret, tuple) else (ret,)
+    if ret[0] != rt.cudaError_t.cudaSuccess:
+        raise RuntimeError(f"CUDA runtime call failed: {ret[0]}")
+    return ret[1] if len(ret) > 1 else None
+
+
 def h2d_peak(bufs, bases, torch, gib=4, reps=5, world=1, gpus=None):
     """B_h2d(N): the copy engine's best host->device rate from the same pinned buffer into
     the same destination over >= 4 GiB: max of one 4 GiB
@@ -486,13 +494,13 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=5, world=1, gpus=None):
                     torch.cuda._sleep(2_000_000)
                     if rt is not None:  # plain cudaMemcpyAsync calls, no framework in the way
                         st = torch.cuda.current_stream(g).cuda_stream
-                        rt.cudaSetDevice(g)
-                        s, e = rt.cudaEventCreate()[1], rt.cudaEventCreate()[1]
-                        rt.cudaEventRecord(s, st)
+                        _rt_ok(rt, rt.cudaSetDevice(g))
+                        s, e = _rt_ok(rt, rt.cudaEventCreate()), _rt_ok(rt, rt.cudaEventCreate())
+                        _rt_ok(rt, rt.cudaEventRecord(s, st))
                         for o in range(0, n, step):
-                            rt.cudaMemcpyAsync(bases[p].data_ptr() + o, bufs[p].ptr + o, min(step, n - o),
-                                               rt.cudaMemcpyKind.cudaMemcpyHostToDevice, st)
-                        rt.cudaEventRecord(e, st)
+                            _rt_ok(rt, rt.cudaMemcpyAsync(bases[p].data_ptr() + o, bufs[p].ptr + o, min(step, n - o),
+                                                          rt.cudaMemcpyKind.cudaMemcpyHostToDevice, st))
+                        _rt_ok(rt, rt.cudaEventRecord(e, st))
                     else:
                         src, dst = bufs[p].torch()[:n], bases[p][:n]
                         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -503,8 +511,8 @@ def h2d_peak(bufs, bases, torch, gib=4, reps=5, world=1, gpus=None):
                 evs.append((s, e))
             if rt is not None:
                 for s, e in evs:
-                    rt.cudaEventSynchronize(e)
-                times = [rt.cudaEventElapsedTime(s, e)[1] for s, e in evs]
+                    _rt_ok(rt, rt.cudaEventSynchronize(e))
+                times = [_rt_ok(rt, rt.cudaEventElapsedTime(s, e)) for s, e in evs]
                 for s, e in evs:
                     rt.cudaEventDestroy(s)
                     rt.cudaEventDestroy(e)
