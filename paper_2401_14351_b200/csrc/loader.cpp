@@ -858,7 +858,14 @@ class WorkerPool {
   void run(std::function<void()> f) {
     std::lock_guard<std::mutex> g(mu_);
     q_.push_back(std::move(f));
-    if (idle_ < q_.size()) std::thread([this] { loop(); }).detach();
+    if (idle_ < q_.size()) {
+      try {
+        std::thread([this] { loop(); }).detach();
+      } catch (...) {  // the job never runs: take it back, the caller fails it
+        q_.pop_back();
+        throw;
+      }
+    }
     cv_.notify_one();
   }
 
@@ -1104,7 +1111,14 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   for (auto& j : L->jobs) {
     sllm_load* Lp = L.get();
     PartJob* jp = &j;
-    worker_pool().run([Lp, jp] { run_job_guarded(Lp, *jp); });
+    try {
+      worker_pool().run([Lp, jp] { run_job_guarded(Lp, *jp); });
+    } catch (const std::exception& e) {  // no thread for this job: it fails, the load stays valid
+      std::lock_guard<std::mutex> g(L->issue_mu);
+      j.status = SLLM_E_INVALID;
+      j.error = std::string("cannot start a load worker thread: ") + e.what();
+      j.issue_signalled = j.finished = true;
+    }
   }
   // Caller-stream ordering without a device-side gate: a stream waiting for work that is not
   // yet enqueued can block, through the few hardware queues the context's streams share,
