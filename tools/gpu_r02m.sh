@@ -14,4 +14,4 @@ for t in memcheck racecheck synccheck; do
 done
 SANITIZE_ONLY=ring timeout 900 compute-sanitizer --tool racecheck --error-exitcode 99 --print-limit 50 python tools/sanitize_gpu.py \
       > $O/sanitizer/racecheck_ring.log 2>&1; echo "rc=$?" >> $O/sanitizer/racecheck_ring.log
-timeout 900 python tools/soak.py --opt-loads 30 --lora-loads 100 > $O/soak.jsonl 2> $O/soak.err
+timeout 900 python tools/soak.py --config opt-6.7b --loads 30 > $O/soak.jsonl 2> $O/soak.err
