@@ -205,7 +205,7 @@ sllm_status sllm_index_tensor(const sllm_index* idx, size_t i, sllm_tensor_info*
     if (i >= idx->tensors.size()) fail(SLLM_E_LOOKUP, "tensor index out of range");
     const TensorRec& t = idx->tensors[i];
     sllm_tensor_info o{};
-    o.name = t.name.c_str();
+    o.name = t.name.data();  // NUL-terminated in the index's name arena
     o.device_id = t.device;
     o.partition = t.part;
     o.dtype = t.dtype;
@@ -220,9 +220,9 @@ sllm_status sllm_index_tensor(const sllm_index* idx, size_t i, sllm_tensor_info*
 sllm_status sllm_index_find(const sllm_index* idx, const char* name, size_t* i) {
   return guard([&] {
     if (!idx || !name || !i) fail(SLLM_E_INVALID, "null argument");
-    auto it = idx->by_name.find(name);
-    if (it == idx->by_name.end()) fail(SLLM_E_LOOKUP, std::string("unknown tensor '") + name + "'");
-    *i = it->second;
+    const uint32_t id = idx->by_name.find(name, idx->tensors);
+    if (id == NameTable::kNone) fail(SLLM_E_LOOKUP, std::string("unknown tensor '") + name + "'");
+    *i = id;
   });
 }
 
@@ -230,9 +230,9 @@ sllm_status sllm_tensor_address(const sllm_index* idx, const char* name, const u
                                 int32_t* device_id, uint64_t* addr) {
   return guard([&] {
     if (!idx || !name || !base_by_partition || !addr) fail(SLLM_E_INVALID, "null argument");
-    auto it = idx->by_name.find(name);
-    if (it == idx->by_name.end()) fail(SLLM_E_LOOKUP, std::string("unknown tensor '") + name + "'");
-    const TensorRec& t = idx->tensors[it->second];
+    const uint32_t id = idx->by_name.find(name, idx->tensors);
+    if (id == NameTable::kNone) fail(SLLM_E_LOOKUP, std::string("unknown tensor '") + name + "'");
+    const TensorRec& t = idx->tensors[id];
     if (device_id) *device_id = t.device;
     *addr = base_by_partition[t.part] + t.offset;  // P:549 base + offset
   });

@@ -43,7 +43,7 @@ bool bind_thread_to_gpu(int gpu);      // ... the node of `gpu`'s PCIe root
 int page_node(const void* p);          // node holding the page at p, -1 if unknown
 
 struct TensorRec {
-  std::string name;
+  std::string_view name;  // NUL-terminated, in the owning index's name arena
   int32_t device;
   int32_t part;      // index into Index::parts
   int32_t dtype;
@@ -62,16 +62,77 @@ struct PartRec {
   std::vector<uint32_t> by_offset;   // tensor ids of this partition sorted by offset
 };
 
+// Name -> tensor id: open addressing over a power-of-two table of (hash, id + 1) slots, the
+// keys being views into the tensor table (one probe array, no node allocation per name: the
+// index parse of an 1,120-tensor adapter spent most of its time in per-name heap work).
+class NameTable {
+ public:
+  static constexpr uint32_t kNone = ~0u;
+  void reserve(size_t n) {
+    size_t cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    slots_.assign(cap, Slot{0, 0});
+    mask_ = cap - 1;
+  }
+  // false if the name is already present
+  bool insert(std::string_view k, uint32_t id, const std::vector<TensorRec>& t) {
+    const uint64_t h = hash(k);
+    for (size_t i = h & mask_;; i = (i + 1) & mask_) {
+      Slot& s = slots_[i];
+      if (!s.id1) {
+        s = Slot{h, id + 1};
+        return true;
+      }
+      if (s.h == h && t[s.id1 - 1].name == k) return false;
+    }
+  }
+  uint32_t find(std::string_view k, const std::vector<TensorRec>& t) const {
+    if (slots_.empty()) return kNone;
+    const uint64_t h = hash(k);
+    for (size_t i = h & mask_;; i = (i + 1) & mask_) {
+      const Slot& s = slots_[i];
+      if (!s.id1) return kNone;
+      if (s.h == h && t[s.id1 - 1].name == k) return s.id1 - 1;
+    }
+  }
+  static uint64_t hash(std::string_view k) {  // 8 bytes per step
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ k.size();
+    size_t i = 0;
+    for (; i + 8 <= k.size(); i += 8) {
+      uint64_t w;
+      std::memcpy(&w, k.data() + i, 8);
+      h = (h ^ w) * 0xBF58476D1CE4E5B9ull;
+      h ^= h >> 31;
+    }
+    uint64_t w = 0;
+    std::memcpy(&w, k.data() + i, k.size() - i);
+    h = (h ^ w) * 0x94D049BB133111EBull;
+    return h ^ (h >> 29);
+  }
+
+ private:
+  struct Slot {
+    uint64_t h;
+    uint32_t id1;  // tensor id + 1 (0 = empty)
+  };
+  std::vector<Slot> slots_;
+  size_t mask_ = 0;
+};
+
 }  // namespace sllm
 
 struct sllm_index {
+  sllm_index() = default;
+  sllm_index(const sllm_index&) = delete;  // the tensor names view `names`
+  sllm_index& operator=(const sllm_index&) = delete;
   uint64_t align = 0, block = 0;
   std::string model_id;
   std::vector<sllm::PartRec> parts;
   std::vector<sllm::TensorRec> tensors;
-  // name -> tensor id; keys view tensors[i].name (the tensor table is sized once, never
-  // reallocated after the names are entered)
-  std::unordered_map<std::string_view, uint32_t> by_name;
+  // every tensor name, NUL-terminated, back to back: reserved once before the names are
+  // appended, so the views in `tensors` stay valid
+  std::string names;
+  sllm::NameTable by_name;  // name -> tensor id
   uint64_t payload = 0;
   uint64_t serial = 0;  // process-unique id (device-side caches key on it)
   bool sealed = false;

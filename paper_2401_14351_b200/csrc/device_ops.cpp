@@ -82,7 +82,7 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   for (uint32_t ti : pr.by_offset) {
     const TensorRec& t = idx->tensors[ti];
     if (!dst_tensor[ti] || (reinterpret_cast<uintptr_t>(dst_tensor[ti]) & 15))
-      fail(SLLM_E_INVALID, "destination of '" + t.name + "' is null or not 16-byte aligned");
+      fail(SLLM_E_INVALID, "destination of '" + std::string(t.name) + "' is null or not 16-byte aligned");
     if (t.offset > cur) segs.push_back(Seg{cur, t.offset - cur, nullptr, 0});
     uint64_t end16 = align_up(t.offset + t.nbytes, 16);
     segs.push_back(Seg{t.offset, end16 - t.offset, static_cast<uint8_t*>(dst_tensor[ti]), t.nbytes});

@@ -135,13 +135,18 @@ sllm_index* plan(const sllm_src_tensor* t, size_t n, uint64_t align, uint64_t bl
   std::vector<int32_t> devs;
   idx->tensors.resize(n);
   idx->by_name.reserve(n);
+  size_t name_bytes = 0;
+  for (size_t i = 0; i < n; ++i) name_bytes += (t[i].name ? std::strlen(t[i].name) : 0) + 1;
+  idx->names.reserve(name_bytes);  // (no reallocation below: the views stay valid)
   for (size_t i = 0; i < n; ++i) {
     const sllm_src_tensor& s = t[i];
     if (!s.name || !s.name[0]) fail(SLLM_E_CONVERSION, "empty tensor name");
     TensorRec& r = idx->tensors[i];
-    r.name = s.name;
-    const std::string& name = r.name;
-    if (!idx->by_name.emplace(std::string_view(r.name), (uint32_t)i).second)
+    const size_t at = idx->names.size(), len = std::strlen(s.name);
+    idx->names.append(s.name, len + 1);
+    r.name = std::string_view(idx->names.data() + at, len);
+    const std::string name(r.name);
+    if (!idx->by_name.insert(r.name, (uint32_t)i, idx->tensors))
       fail(SLLM_E_CONVERSION, "duplicate tensor name '" + name + "'");
     int w = dtype_width(s.dtype);
     if (!w) fail(SLLM_E_CONVERSION, "unknown dtype for '" + name + "'");
@@ -224,9 +229,9 @@ void convert_into(const sllm_src_tensor* t, size_t n, sllm_index* idx, void* con
     if (!part_bufs[p]) fail(SLLM_E_INVALID, "null partition buffer");
   for (size_t i = 0; i < n; ++i) {
     const TensorRec& r = idx->tensors[i];
-    if (std::strcmp(t[i].name ? t[i].name : "", r.name.c_str()) || t[i].nbytes != r.nbytes)
+    if (std::strcmp(t[i].name ? t[i].name : "", r.name.data()) || t[i].nbytes != r.nbytes)
       fail(SLLM_E_CONVERSION, "tensor " + std::to_string(i) + " differs from the plan");
-    if (!t[i].data) fail(SLLM_E_INVALID, "null data for '" + r.name + "'");
+    if (!t[i].data) fail(SLLM_E_INVALID, "null data for '" + std::string(r.name) + "'");
   }
   const uint64_t B = idx->block ? idx->block : (4ull << 20);  // work unit: one checksum block
   struct Job { size_t p; uint64_t j; };
@@ -338,6 +343,11 @@ std::vector<uint8_t> serialize(const sllm_index& idx) {
 
 static bool valid_utf8(const uint8_t* s, size_t n) {
   size_t i = 0;
+  for (; i + 8 <= n; i += 8) {  // ASCII fast path, 8 bytes at a time
+    uint64_t w;
+    std::memcpy(&w, s + i, 8);
+    if (w & 0x8080808080808080ull) break;
+  }
   while (i < n) {
     uint8_t c = s[i];
     size_t k;
@@ -411,13 +421,17 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
   if ((uint64_t)n_tensors * 32 > r.limit - r.pos) fail(SLLM_E_FORMAT, "tensor count exceeds the index length");
   idx->tensors.reserve(n_tensors);
   idx->by_name.reserve(n_tensors);
+  idx->names.reserve(r.limit - r.pos);  // every name (+ its NUL) fits the bytes left: no reallocation
   for (uint32_t i = 0; i < n_tensors; ++i) {
     TensorRec t{};
     uint32_t nl = r.get<uint32_t>();
     if (nl == 0) fail(SLLM_E_FORMAT, "empty tensor name");
     const uint8_t* nm = r.take(nl);
     if (!valid_utf8(nm, nl)) fail(SLLM_E_FORMAT, "tensor name not UTF-8");
-    t.name.assign((const char*)nm, nl);
+    const size_t at = idx->names.size();
+    idx->names.append((const char*)nm, nl);
+    idx->names.push_back('\0');
+    t.name = std::string_view(idx->names.data() + at, nl);
     t.device = r.get<int32_t>();
     t.dtype = r.get<uint8_t>();
     t.ndim = r.get<uint8_t>();
@@ -425,7 +439,7 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
     t.offset = r.get<uint64_t>();
     t.nbytes = r.get<uint64_t>();
     auto it = part_of.find(t.device);
-    if (it == part_of.end()) fail(SLLM_E_FORMAT, "tensor '" + t.name + "' on an unknown device");
+    if (it == part_of.end()) fail(SLLM_E_FORMAT, "tensor '" + std::string(t.name) + "' on an unknown device");
     t.part = it->second;
     int w = dtype_width(t.dtype);
     if (!w) fail(SLLM_E_FORMAT, "unknown dtype code");
@@ -433,20 +447,20 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
     unsigned __int128 numel = 1;
     for (int k = 0; k < t.ndim; ++k) {
       t.shape[k] = r.get<int64_t>();
-      if (t.shape[k] <= 0) fail(SLLM_E_FORMAT, "non-positive dimension in '" + t.name + "'");
+      if (t.shape[k] <= 0) fail(SLLM_E_FORMAT, "non-positive dimension in '" + std::string(t.name) + "'");
       numel *= (uint64_t)t.shape[k];
       if (numel >> 62) fail(SLLM_E_FORMAT, "tensor too large");
     }
     r.pad8();
-    if (numel * (unsigned)w != (unsigned __int128)t.nbytes) fail(SLLM_E_FORMAT, "size of '" + t.name + "' != prod(shape) * width");
-    if (t.offset % A) fail(SLLM_E_FORMAT, "offset of '" + t.name + "' not aligned");
+    if (numel * (unsigned)w != (unsigned __int128)t.nbytes) fail(SLLM_E_FORMAT, "size of '" + std::string(t.name) + "' != prod(shape) * width");
+    if (t.offset % A) fail(SLLM_E_FORMAT, "offset of '" + std::string(t.name) + "' not aligned");
     const PartRec& pr = idx->parts[t.part];
-    if (t.offset > pr.length || t.nbytes > pr.length - t.offset) fail(SLLM_E_FORMAT, "'" + t.name + "' extends past its partition");
+    if (t.offset > pr.length || t.nbytes > pr.length - t.offset) fail(SLLM_E_FORMAT, "'" + std::string(t.name) + "' extends past its partition");
     count[t.part]++;
     sum += t.nbytes;
-    idx->tensors.push_back(std::move(t));  // (reserved: no reallocation, the name views stay valid)
-    const std::string& nmv = idx->tensors.back().name;
-    if (!idx->by_name.emplace(std::string_view(nmv), i).second) fail(SLLM_E_FORMAT, "duplicate tensor name '" + nmv + "'");
+    idx->tensors.push_back(t);
+    if (!idx->by_name.insert(t.name, i, idx->tensors))
+      fail(SLLM_E_FORMAT, "duplicate tensor name '" + std::string(t.name) + "'");
   }
   for (uint32_t p = 0; p < n_parts; ++p)
     if (count[p] != idx->parts[p].n_tensors) fail(SLLM_E_FORMAT, "partition tensor count mismatch");
@@ -457,7 +471,7 @@ sllm_index* parse(const uint8_t* blob, size_t n) {
     for (size_t k = 1; k < pr.by_offset.size(); ++k) {
       const TensorRec& a = idx->tensors[pr.by_offset[k - 1]];
       const TensorRec& b = idx->tensors[pr.by_offset[k]];
-      if (b.offset < a.offset + a.nbytes) fail(SLLM_E_FORMAT, "overlapping tensors '" + a.name + "' and '" + b.name + "'");
+      if (b.offset < a.offset + a.nbytes) fail(SLLM_E_FORMAT, "overlapping tensors '" + std::string(a.name) + "' and '" + std::string(b.name) + "'");
     }
   {  // the checksum tables must fit the bytes left before the trailer (n_blocks comes from L_d)
     unsigned __int128 need = 0;

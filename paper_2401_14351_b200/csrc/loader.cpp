@@ -1037,9 +1037,9 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
     if (j.dst_base && (reinterpret_cast<uintptr_t>(j.dst_base) & 15)) fail(SLLM_E_INVALID, "dst_base must be 16-byte aligned");
     if (scatter) {
       for (uint32_t ti : idx->parts[p].by_offset) {
-        if (!dst_tensor[ti]) fail(SLLM_E_INVALID, "null destination for tensor '" + idx->tensors[ti].name + "'");
+        if (!dst_tensor[ti]) fail(SLLM_E_INVALID, "null destination for tensor '" + std::string(idx->tensors[ti].name) + "'");
         if (reinterpret_cast<uintptr_t>(dst_tensor[ti]) & 15)
-          fail(SLLM_E_INVALID, "destination of '" + idx->tensors[ti].name + "' is not 16-byte aligned");
+          fail(SLLM_E_INVALID, "destination of '" + std::string(idx->tensors[ti].name) + "' is not 16-byte aligned");
       }
     }
     SLLM_CUDA(cudaSetDevice(j.gpu));
@@ -1218,19 +1218,19 @@ sllm_status sllm_load_wait_internal(sllm_load* L, sllm_load_report* rep) {
 
 void sllm_load_tensor_internal(const sllm_load* L, const char* name, sllm_tensor_handle* h) {
   if (!name || !h) fail(SLLM_E_INVALID, "null argument");
-  auto it = L->idx->by_name.find(name);
-  if (it == L->idx->by_name.end()) fail(SLLM_E_LOOKUP, std::string("unknown tensor '") + name + "'");
-  const TensorRec& t = L->idx->tensors[it->second];
+  const uint32_t id = L->idx->by_name.find(name, L->idx->tensors);
+  if (id == NameTable::kNone) fail(SLLM_E_LOOKUP, std::string("unknown tensor '") + name + "'");
+  const TensorRec& t = L->idx->tensors[id];
   const PartJob* job = nullptr;
   for (auto& j : L->jobs)
     if ((int32_t)j.p == t.part) job = &j;
-  if (!job) fail(SLLM_E_LOOKUP, "tensor '" + t.name + "' belongs to a partition this load does not handle");
+  if (!job) fail(SLLM_E_LOOKUP, "tensor '" + std::string(t.name) + "' belongs to a partition this load does not handle");
   sllm_tensor_handle o{};
   o.gpu = job->gpu;
   o.dtype = t.dtype;
   o.ndim = t.ndim;
   std::memcpy(o.shape, t.shape, sizeof o.shape);
-  o.ptr = L->dst_tensor.empty() ? (void*)(job->dst_base + t.offset) : L->dst_tensor[it->second];
+  o.ptr = L->dst_tensor.empty() ? (void*)(job->dst_base + t.offset) : L->dst_tensor[id];
   o.nbytes = t.nbytes;
   *h = o;
 }
