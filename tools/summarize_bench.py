@@ -15,6 +15,8 @@ def main():
         c = d["config"]
         r = d.get("roofline") or {}
         kern = f"{r['frac']:.3f} of {r['bound']}" if r.get("frac") is not None else "—"
+        if (r.get("in_kernel") or {}).get("frac"):
+            kern += f" ({r['in_kernel']['frac']:.3f} in-kernel)"
         cpu = d.get("cpu_baseline") or {}
         print(f"| {c['workload']} | {c['mode']} | {c['fanout']} | {c['partitions_per_gpu']} "
               f"| {c['payload_bytes_per_gpu'] / 1e9:.2f} | {d['time_to_loaded_model_s']:.4f} | {d['value']:.2f} "
