@@ -8,6 +8,7 @@ checksums, which the CPU suite pins to the oracle (tests/test_format_parity.py).
 """
 from __future__ import annotations
 
+import os
 from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
 from synth import models, payload
@@ -38,6 +39,8 @@ def build_pinned(inv: Sequence[models.TensorSpec], seed: int, align: int = 4096,
             ptrs.append(bufs[t.partition].ptr + t.offset)
             sizes.append(t.nbytes)
             es.append(e)
+    if not threads:  # ranks of one node share its cores (8 ranks each building 17 GB at once)
+        threads = max(1, len(os.sched_getaffinity(0)) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))
     payload.payload_into(ptrs, sizes, seed, es, threads)
     idx.seal([bufs[p].ptr if p in bufs else None for p in range(len(parts))])
     return idx, bufs
