@@ -970,6 +970,10 @@ def main(argv=None):
                                  "what": "%globaltimer span of each launch; the CUDA-event time also holds the launch "
                                          "and completion, which cost ~30 us each while the copy engine saturates "
                                          "PCIe (profiles/r02/launch_gap.jsonl)"}
+        if replicated and world > 1:
+            roof["note"] = ("replicated load: the fan-out launches also store every byte they read into the "
+                            f"{world - 1} peer replica(s) (NVLink; here counted as reads only) and the received "
+                            "ranges are verified by K4 launches -- see roofline_nvlink for the fan-out's rate")
     if args.mode in ("zerocopy", "scatter_zc") and kern_launches and kern_ms > 0:
         # zero-copy kernel: every byte it reads crosses PCIe -> bound by the host link.
         # Launches on the S streams overlap, so the kernel's rate is its bytes per step
