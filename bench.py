@@ -961,7 +961,7 @@ def main(argv=None):
                 ("checksum only" if args.mode == "ce" else "scatter+checksum"),
                 "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
                 "bytes_per_launch": per_launch_bytes,
-                "note": "one CTA per SM, units handed out by ticket; each launch verifies a span of landed windows "
+                "note": "two CTAs per SM, units handed out by ticket; each launch verifies a span of landed windows "
                         "(up to 4 GiB, shrinking towards the end) beside the PCIe copies"}
         span_ms = sum(r.get("t_kernel_span_ms_sum", 0.0) for r in reports) / len(reports)
         if span_ms > 0:  # the same launches timed from inside (first CTA start .. last CTA end)

@@ -20,13 +20,6 @@ static int standalone_engine() {
   fail(SLLM_E_INVALID, std::string("SLLM_STANDALONE_ENGINE: unknown engine '") + e + "'");
 }
 
-static int default_grid() {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;  // one resident 256-thread CTA per SM (145-152 registers per thread)
-}
-
 void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint64_t* out, int ctas,
                             cudaStream_t st) {
   if (!src || !out || !block) fail(SLLM_E_INVALID, "null argument");
@@ -61,7 +54,7 @@ void block_checksums_device(const void* src, uint64_t len, uint64_t block, uint6
   if (!getenv("SLLM_STATIC_UNITS")) mp.ticket = ticket;  // dynamic unit distribution (base 0)
   static const bool ktime = getenv("SLLM_KTIME") != nullptr;  // diagnostic: in-kernel span on stderr
   if (ktime) mp.ktime = reinterpret_cast<unsigned long long*>(b + acc_bytes + 320);
-  SLLM_CUDA(launch_materialise(mp, MatKind::kChecksumOnly, ctas > 0 ? ctas : default_grid(), st));
+  SLLM_CUDA(launch_materialise(mp, MatKind::kChecksumOnly, ctas > 0 ? ctas : 0, st));
   if (ktime) {
     unsigned long long kt[4];
     SLLM_CUDA(cudaMemcpyAsync(kt, mp.ktime, sizeof(kt), cudaMemcpyDeviceToHost, st));
@@ -133,7 +126,7 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
   if (kernel_ms)
     for (auto& e : ev) SLLM_CUDA(cudaEventCreate(&e));
   if (kernel_ms) SLLM_CUDA(cudaEventRecord(ev[0], st));
-  SLLM_CUDA(launch_materialise(mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas > 0 ? ctas : default_grid(), st));
+  SLLM_CUDA(launch_materialise(mp, check ? MatKind::kCopyChecksum : MatKind::kCopyOnly, ctas > 0 ? ctas : 0, st));
   if (kernel_ms) SLLM_CUDA(cudaEventRecord(ev[1], st));
   unsigned long long bad = ~0ull;
   SLLM_CUDA(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st));

@@ -210,13 +210,14 @@ __global__ void __launch_bounds__(kThreads) materialise_kernel(const MatParams p
 
 
 // ---------------------------------------------------------------------------------
-// TMA-staged variant (default engine).  One CTA = 1 producer warp + 8 consumer warps.
-// The producer streams the CTA's blocks through a 12-stage shared-memory ring with
-// 1-D bulk copies (cp.async.bulk, completion counted on an mbarrier); the consumers
-// read each 16 KiB stage with 16-byte LDS, store the tensor bytes to their destination
-// and accumulate the closed-form checksum terms.  A CTA owns whole checksum blocks, so
-// a block is reduced once inside the CTA -- no global atomics, no fences.  192 KiB in
-// flight per SM covers HBM latency (K3/K4) and, with a few CTAs, PCIe latency (K2).
+// TMA-staged variant (default engine).  One CTA = 1 producer warp + 8 consumer warps (+ a
+// bulk-storer warp for engine 2), two CTAs per SM.  The producer streams the CTA's units
+// through a 6-stage shared-memory ring with 1-D bulk copies (cp.async.bulk, completion
+// counted on an mbarrier); the consumers read each 16 KiB stage with 16-byte LDS, store the
+// tensor bytes to their destination and accumulate the closed-form checksum terms.  A CTA
+// owns whole checksum blocks unless a launch splits them, so a block is usually reduced
+// once inside the CTA -- no global atomics, no fences.  192 KiB in flight per SM covers HBM
+// latency (K3/K4) and PCIe latency (K2).
 // ---------------------------------------------------------------------------------
 constexpr int kConsumerWarps = 8;
 // Stage release: one arrival per consumer warp after __syncwarp (default), or one per
@@ -237,8 +238,21 @@ constexpr int kStoreLag = 4;                             // bulk-store groups in
 #define SLLM_STAGE_KIB 16
 #endif
 constexpr int kConsumerUnroll = SLLM_CONSUMER_UNROLL;
-constexpr uint32_t kStageBytes = SLLM_STAGE_KIB << 10;  // ring: kStages x kStageBytes = 192 KiB
-constexpr int kStages = (192 << 10) / kStageBytes;
+// Ring bytes per CTA and CTAs per SM (A/B knobs SLLM_RING_KIB / SLLM_CTAS_PER_SM).  Two CTAs
+// per SM with 96 KiB rings (the same bytes in flight per SM as one 192 KiB ring) beat one:
+// while one CTA's consumers meet at a unit end or its producer waits, the other streams --
+// K4 0.620 -> 0.586 ms per 4 GiB, K3 4.24 -> 4.01 ms per 26.6 GB (ncu), in-pipeline K4
+// 0.955 -> 0.985 and K3 0.834 -> 0.88 by events; three 64 KiB CTAs measure the same as two
+// (profiles/r02/ctas_per_sm/).
+#ifndef SLLM_RING_KIB
+#define SLLM_RING_KIB 96
+#endif
+#ifndef SLLM_CTAS_PER_SM
+#define SLLM_CTAS_PER_SM 2
+#endif
+constexpr int kCtasPerSm = SLLM_CTAS_PER_SM;
+constexpr uint32_t kStageBytes = SLLM_STAGE_KIB << 10;  // ring: kStages x kStageBytes
+constexpr int kStages = (SLLM_RING_KIB << 10) / kStageBytes;
 constexpr uint64_t kMaxUnitBytes = 1ull << 20;  // default: whole 1 MiB blocks when the launch is balanced
 constexpr uint32_t kFineTail = 4;  // fine-tail units per block (see launch_tma)
 constexpr size_t kTmaSmem = (size_t)kStages * kStageBytes + 2 * kStages * sizeof(uint64_t);
@@ -362,7 +376,7 @@ __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;"
 // kMc: the NVLS fan-out's instance (every vector stored once through the multicast address;
 // a separate instance keeps the per-vector test out of the K2 / K3 store loops)
 template <bool kStore, bool kCheck, bool kMc = false>
-__global__ void __launch_bounds__(kTmaThreads, 1) materialise_tma_kernel(const MatParams p) {
+__global__ void __launch_bounds__(kTmaThreads, kCtasPerSm) materialise_tma_kernel(const MatParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kStageBytes);
   uint64_t* empty = full + kStages;
@@ -665,38 +679,40 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream,
 #endif
     configured[dev & 63].store(true, std::memory_order_release);
   }
-  // Split checksum blocks into up to 16 units of >= one stage (16 KiB) while the launch
-  // has fewer than two units per SM, so a 64 MiB window still covers every SM.
+  // Work items of the launch (see Items): unit size (split), fine tail, ticket count.
   MatParams q = p;
   const uint64_t blk = kCheck ? p.block : (1ull << 20);
-  const int sms = num_sms();
-  const uint64_t G = (uint64_t)(grid < 1 ? sms : grid);
+  const uint64_t G = (uint64_t)(grid < 1 ? num_sms() * kCtasPerSm : grid);  // resident CTAs
   q.split = 1;
   const uint64_t blocks = (p.hi + blk - 1) / blk - p.lo / blk;
   auto can_halve = [&](uint32_t s) { return s < 16 && blk / (2 * s) >= kStageBytes && (blk / (2 * s)) % 16 == 0; };
-  while (can_halve(q.split) && blocks * q.split < 2ull * sms) q.split *= 2;
   // Wave balance: a launch of U equal units on G CTAs runs ceil(U/G) waves, the last one
-  // U/G - floor(U/G) full -- e.g. a 397-block span on 148 SMs runs 2.68 of 3 waves (89 %).
+  // U/G - floor(U/G) full -- e.g. a 397-block span on 148 CTAs runs 2.68 of 3 waves (89 %).
   auto balance = [&](uint32_t s) {
     const uint64_t U = blocks * s;
     return (double)U / (double)(((U + G - 1) / G) * G);
   };
-  // Fine tail (SLLM_FINE_TAIL=0 turns it off: A/B knob): a launch of >= 2 waves of whole
-  // blocks whose last wave is < 95 % full hands out its last G blocks in quarter blocks
-  // instead of splitting every block, so only the end pays the per-piece combine.  In-kernel
-  // spans (profiles/r02/fine_tail/, r02v): 470 MB (448 blocks, 76 % last wave) 0.113 ms with
-  // every block in eighths vs 0.084 with the fine tail; balanced launches are faster without
-  // it (4 GiB: 0.6125 vs 0.6166 ms; 576 blocks: 0.093 vs 0.102 ms).
-  static const bool fine_on = [] {
+  // Fine tail: a launch of >= one wave of whole blocks hands out its last G blocks in
+  // quarter blocks (combined per block like split units) instead of splitting every block,
+  // so the CTAs, which finish their whole blocks up to a block-time apart (~44 us per 1 MiB
+  // at two CTAs per SM), share the end in small pieces.  Measured with two CTAs per SM
+  // (profiles/r02/ctas_per_sm/): 4 GiB K4 span 0.5855 -> 0.5806 ms, K3 4.009 -> 3.997 ms
+  // (ncu), in-pipeline K4 0.996 -> 1.005 by events; the 470 MB LoRA span (448 blocks on 296
+  // CTAs) 0.095 ms with every block in sixteenths -> 0.075.  (With one CTA per SM the tail
+  // only paid off on unbalanced launches: SLLM_FINE_TAIL=1 keeps that rule, 0 turns it off.)
+  static const int fine_mode = [] {  // 0 off, 1 unbalanced launches only, 2 every launch (default)
     const char* e = getenv("SLLM_FINE_TAIL");
-    return !(e && atoi(e) == 0);
+    return e ? atoi(e) : 2;
   }();
-  const bool tail = fine_on && q.split == 1 && blocks >= 2 * G && balance(1) < 0.95 &&
+  const bool tail = fine_mode && blocks >= G && (fine_mode == 2 || balance(1) < 0.95) &&
                     blk / kFineTail >= (64u << 10) && (blk / kFineTail) % kStageBytes == 0;
-  // Otherwise keep halving the unit (down to 64 KiB) until the last wave is >= 95 % full
-  // (the 397-block span: 97.5 % at split 4).
-  if (!tail)
+  if (!tail) {
+    // fewer blocks than CTAs, or balanced: split blocks into up to 16 units of >= one stage
+    // while the launch has fewer than two units per CTA (so a 64 MiB window still covers
+    // every SM), then keep halving (down to 64 KiB) until the last wave is >= 95 % full
+    while (can_halve(q.split) && blocks * q.split < 2ull * G) q.split *= 2;
     while (can_halve(q.split) && blk / (2 * q.split) >= (64u << 10) && balance(q.split) < 0.95) q.split *= 2;
+  }
   // Largest unit (measurement knob SLLM_UNIT_KIB): smaller units shorten the launch's tail
   // (the last CTA to finish is at most one unit behind) at 4 atomics per unit.
   static const uint64_t max_unit = [] {
@@ -724,7 +740,7 @@ static cudaError_t launch_tma(const MatParams& p, int grid, cudaStream_t stream,
 cudaError_t launch_materialise(const MatParams& p, MatKind kind, int grid, cudaStream_t stream, uint64_t* tickets) {
   if (tickets) *tickets = 0;
   if (p.hi <= p.lo) return cudaSuccess;
-  if (grid < 1) grid = num_sms();  // default: one CTA per SM
+  if (grid < 1) grid = num_sms() * (p.engine >= 1 ? kCtasPerSm : 1);  // default: one (ring) CTA per SM
   if (p.engine >= 1) {
     switch (kind) {
       case MatKind::kChecksumOnly: return launch_tma<false, true>(p, grid, stream, tickets);

@@ -223,7 +223,7 @@ static uint32_t tile_for(const sllm_index& idx) {
   return idx.block ? (uint32_t)std::min<uint64_t>(kTile, idx.block) : kTile;
 }
 
-// 0 = one CTA per SM (resolved by launch_materialise): every window's kernel spreads
+// 0 = one grid of ring CTAs per GPU (two per SM, resolved by launch_materialise): every window's kernel spreads
 // over the whole GPU, splitting checksum blocks across CTAs when a window is small.
 static int default_ctas(int /*mode*/) { return 0; }
 

@@ -1,5 +1,6 @@
 """GPU parity of the ring kernel's work distributions: dynamic units (tickets)
-with the fine tail (the default), dynamic units without the fine tail (SLLM_FINE_TAIL=0),
+with the fine tail on every launch (the default) or on unbalanced launches only
+(SLLM_FINE_TAIL=1), dynamic units without the fine tail (SLLM_FINE_TAIL=0),
 the static schedule (SLLM_STATIC_UNITS=1) and both knobs together.  The knobs are read once
 per process, so each combination runs in a child process that
 
@@ -61,9 +62,9 @@ print("schedule-child ok")
 """
 
 
-@pytest.mark.parametrize("env", [{}, {"SLLM_FINE_TAIL": "0"}, {"SLLM_STATIC_UNITS": "1"},
+@pytest.mark.parametrize("env", [{}, {"SLLM_FINE_TAIL": "1"}, {"SLLM_FINE_TAIL": "0"}, {"SLLM_STATIC_UNITS": "1"},
                                  {"SLLM_STATIC_UNITS": "1", "SLLM_FINE_TAIL": "0"}],
-                         ids=["dynamic+fine", "dynamic", "static+fine", "static"])
+                         ids=["dynamic+fine", "dynamic+fine-unbalanced", "dynamic", "static+fine", "static"])
 def test_work_distribution_parity(env):
     e = dict(os.environ)
     e.pop("SLLM_FINE_TAIL", None)
