@@ -781,6 +781,9 @@ def main(argv=None):
         import torch.distributed as dist
         if not SAME_GPU and visible_gpus() < world:
             fail_loudly(f"{world} ranks need {world} visible GPUs, found {visible_gpus()}")
+        if SAME_GPU and args.fanout == "p2p":  # ranks as processes wait on each other's device-side flags
+            fail_loudly("--fanout p2p with one process per rank needs one GPU per rank (its kernels wait on "
+                        "the peers' flags); SLLM_BENCH_SAME_GPU covers the sharded and NCCL paths only")
         torch.cuda.set_device(gpu_of(local))
         if SAME_GPU:
             dist.init_process_group("gloo")

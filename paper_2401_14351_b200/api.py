@@ -80,8 +80,10 @@ def _ptr_array(ptrs: Iterable[Optional[int]]) -> C.Array:
 # plans), shared by every Index parsed from the same bytes: the C parse and validation (a1)
 # still run for every Index, but the per-tensor Python objects are built once per content
 # instead of once per load (a latency-bound load of a 1,120-tensor LoRA adapter otherwise
-# spends ~1 ms per step creating and tearing them down).  Keyed by the index trailer
-# (Fletcher-64 of every preceding byte + total length); bounded LRU.
+# spends ~1 ms per step creating and tearing them down).  Keyed by the index bytes
+# themselves (a checksum key could map two different indexes to one table: Fletcher-64 does
+# not tell a 0x00000000 word from 0xFFFFFFFF); the hash of a bytes object is cached on it,
+# so a caller re-opening the same blob pays one hash; bounded LRU.
 _DERIVED: "Dict[bytes, dict]" = {}
 _DERIVED_MAX = 16
 
@@ -128,7 +130,7 @@ class Index:
         blob = bytes(blob)
         out = C.c_void_p()
         check(lib().sllm_index_from_memory(blob, len(blob), C.byref(out)))
-        return cls(out.value, key=blob[-16:])
+        return cls(out.value, key=blob)
 
     def close(self) -> None:
         if self._h and self._h.value:

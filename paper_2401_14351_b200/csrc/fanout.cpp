@@ -66,21 +66,25 @@ static void nccl_check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) fail(SLLM_E_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
 }
 
-// Ranks of one P2P group that live in the same process (tests, several replicas on one
-// GPU) share one CUDA context, whose streams are multiplexed onto a few hardware work
-// queues.  A rank's device-side peer wait sits at the head of its queue until the peers
-// signal; a peer's work submitted to the same hardware queue *after* that wait would be
-// stuck behind it -- a false dependency that only the timeout breaks.  So in-process ranks
-// rendezvous on the host at two points of every load: after each has queued its ready
-// signal (before anyone queues the ready wait) and after each has queued its done signal
-// (before the next load's done wait).  Everything a wait depends on is then queued ahead
-// of it in every hardware queue.  One rank per process (the deployment) skips this.
+// Ranks of one P2P group that live in the same process (several GPUs driven by one process,
+// or tests with several replicas on one GPU) order each other with CUDA events instead of
+// device-side flag waits: rank r records its `ready` event once its stores into every replica
+// are done and its `done` event once it has verified what it received, and a peer's stream
+// waits on those events (cudaStreamWaitEvent, across devices too).  No kernel of one rank
+// then waits for a kernel of another, so the ranks may share a GPU -- kernels that spin on a
+// flag another rank writes must not (nothing guarantees both run at once; on B200 such
+// ranks as processes on one GPU raised Xid 109).  An event wait only orders after the
+// record already queued, so the in-process ranks rendezvous on the host at two points of
+// every load: after each has recorded `ready` (before anyone waits on it) and after each
+// has recorded `done` (before the next load's wait on it).  One rank per process (the
+// deployment, peers mapped with CUDA IPC) uses the device-side signals instead.
 struct LocalGroup {
   std::mutex mu;
   std::condition_variable cv;
   int members = 0;
   int count = 0;
   uint64_t gen = 0;
+  std::vector<cudaEvent_t> ev[2];  // [kPeerReady / kPeerDone][rank], owned by the rank's handle
 };
 static std::mutex g_groups_mu;
 static std::map<std::vector<uint32_t*>, std::weak_ptr<LocalGroup>> g_groups;
@@ -100,6 +104,7 @@ struct sllm_comm {
   uint64_t timeout_ns = 0;
   cudaStream_t streams[sllm::kMaxStreams + 1] = {};
   std::shared_ptr<sllm::LocalGroup> local;  // the in-process ranks of this peer group
+  cudaEvent_t ev[2] = {};                    // this rank's ready / done events (in-process groups)
   // NVLS group (SLLM_FANOUT_NVLS): the multicast object and the library-owned replicas it
   // binds (shared by the group's handles); mc = the multicast address of replica byte 0
   std::shared_ptr<sllm::NvlsGroup> nvls;
@@ -125,21 +130,55 @@ uint32_t comm_next_epoch(sllm_comm* c) {
   if (++c->epoch == 0) ++c->epoch;  // 0 is the signal arrays' initial value
   return c->epoch;
 }
-void comm_local_barrier(sllm_comm* c) {
+bool comm_in_process(const sllm_comm* c) {
+  if (!c || !c->local || c->nranks < 2) return false;
+  std::lock_guard<std::mutex> g(c->local->mu);
+  return c->local->members == c->nranks;
+}
+
+void comm_record(sllm_comm* c, PeerEvent which, cudaStream_t s) { SLLM_CUDA(cudaEventRecord(c->ev[which], s)); }
+
+void comm_wait_peers(sllm_comm* c, PeerEvent which, cudaStream_t s) {
+  std::vector<cudaEvent_t> evs;
+  {
+    std::lock_guard<std::mutex> g(c->local->mu);
+    evs = c->local->ev[which];
+  }
+  for (int q = 0; q < (int)evs.size(); ++q)
+    if (q != c->rank) {
+      if (!evs[q]) fail(SLLM_E_PEER, "peer rank " + std::to_string(q) + " of this process has no handle");
+      SLLM_CUDA(cudaStreamWaitEvent(s, evs[q], 0));
+    }
+}
+
+bool comm_local_barrier(sllm_comm* c) {
   LocalGroup* g = c->local.get();
-  if (!g) return;
+  if (!g) return true;
   std::unique_lock<std::mutex> lk(g->mu);
-  if (g->members <= 1) return;
+  if (g->members <= 1) return true;
   const uint64_t my = g->gen;
   if (++g->count == g->members) {
     g->count = 0;
     ++g->gen;
     g->cv.notify_all();
-    return;
+    return true;
   }
-  // a rank that never arrives (its load was not started): give up after the group timeout;
-  // the device-side wait then reports SLLM_E_PEER
-  if (!g->cv.wait_for(lk, std::chrono::nanoseconds(c->timeout_ns), [&] { return g->gen != my; })) --g->count;
+  // a rank that never arrives (its load was not started): give up after the group timeout
+  if (!g->cv.wait_for(lk, std::chrono::nanoseconds(c->timeout_ns), [&] { return g->gen != my; })) {
+    --g->count;
+    return false;
+  }
+  return true;
+}
+
+// This rank's share of the in-process group's events (created on the rank's GPU, current).
+static void join_local_events(sllm_comm* c) {
+  for (int w = 0; w < 2; ++w) SLLM_CUDA(cudaEventCreateWithFlags(&c->ev[w], cudaEventDisableTiming));
+  std::lock_guard<std::mutex> lg(c->local->mu);
+  for (auto& v : c->local->ev) {
+    if ((int)v.size() < c->nranks) v.resize(c->nranks, nullptr);
+  }
+  for (int w = 0; w < 2; ++w) c->local->ev[w][c->rank] = c->ev[w];
 }
 
 cudaStream_t comm_stream(sllm_comm* c, int s) {  // s = 0..kMaxStreams-1 transfer, kMaxStreams = kernel
@@ -250,8 +289,11 @@ sllm_comm* sllm_comm_init_peers_internal(int32_t nranks, int32_t rank, int32_t g
     auto& w = g_groups[c->signal];
     c->local = w.lock();
     if (!c->local) w = c->local = std::make_shared<LocalGroup>();
-    std::lock_guard<std::mutex> lg(c->local->mu);
-    ++c->local->members;
+    {
+      std::lock_guard<std::mutex> lg(c->local->mu);
+      ++c->local->members;
+    }
+    join_local_events(c.get());
   }
   return c.release();
 }
@@ -279,7 +321,11 @@ void sllm_comm_init_nvls_internal(const int32_t* gpus, int32_t n, uint64_t bytes
     }
     c->nvls = g;
     c->mc = nvls_mc(*g);
-    if (n > 1) c->local = local;
+    if (n > 1) {
+      c->local = local;
+      SLLM_CUDA(cudaSetDevice(gpus[i]));
+      join_local_events(c.get());
+    }
     cs.push_back(std::move(c));
   }
   for (int i = 0; i < n; ++i) out[i] = cs[i].release();
@@ -295,6 +341,11 @@ void sllm_comm_replica_internal(const sllm_comm* c, void** base, uint64_t* bytes
 void sllm_comm_free_internal(sllm_comm* c) {
   if (!c) return;
   if (c->comm && g_nccl_ok) g_nccl.CommDestroy(c->comm);
+  if (c->local) {  // this rank's events leave the group's table (its loads are complete)
+    std::lock_guard<std::mutex> lg(c->local->mu);
+    for (auto& v : c->local->ev)
+      if (c->rank < (int)v.size() && (v[c->rank] == c->ev[0] || v[c->rank] == c->ev[1])) v[c->rank] = nullptr;
+  }
   if (c->local && c->nvls) {  // (an NVLS group's local share is not in the registry)
     std::lock_guard<std::mutex> lg(c->local->mu);
     --c->local->members;
@@ -315,6 +366,8 @@ void sllm_comm_free_internal(sllm_comm* c) {
         cudaStreamSynchronize(s);
         cudaStreamDestroy(s);
       }
+    for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
   }
   delete c;
 }

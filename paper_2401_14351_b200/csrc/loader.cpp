@@ -613,11 +613,16 @@ static void run_job(sllm_load* L, PartJob& j) {
   SLLM_CUDA(cudaMemcpyAsync(base, h, up_bytes, cudaMemcpyHostToDevice, s0));
   SLLM_CUDA(cudaMemsetAsync(base + up_bytes, 0, zero_bytes, s0));
   SLLM_CUDA(cudaEventRecord(j.ev[0], s0));
+  const bool in_process = p2p && comm_in_process(L->comm);  // peers ordered by events, not device waits
   if (p2p) {  // no store into a peer replica before every peer is done verifying the previous load
     const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
-    SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me) + R, R, me, j.epoch - 1, comm_timeout_ns(L->comm),
-                               j.d_err, s0));
-    if (R > 1) j.launches++;
+    if (in_process) {
+      comm_wait_peers(L->comm, kPeerDone, s0);
+    } else {
+      SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me) + R, R, me, j.epoch - 1, comm_timeout_ns(L->comm),
+                                 j.d_err, s0));
+      if (R > 1) j.launches++;
+    }
   }
   SLLM_CUDA(cudaEventRecord(j.ev[2], s0));
   for (int s = 1; s < P.S; ++s) SLLM_CUDA(cudaStreamWaitEvent(P.xfer[s], j.ev[2], 0));
@@ -722,23 +727,34 @@ static void run_job(sllm_load* L, PartJob& j) {
     // completed into q's replica, done[r] = last epoch rank r has finished (its replica is
     // free for the next epoch's stores).  Every store of this rank's kernels -> visible to
     // the peers (ready), then wait for theirs, verify what arrived, publish done.
+    // (In-process ranks: the same protocol with CUDA events, see fanout.cpp.)
     PeerSignal ready{}, done{};
     for (int q = 0; q < R; ++q)
       if (q != me) {
         ready.remote[ready.n++] = comm_peer_signal(L->comm, q) + me;
         done.remote[done.n++] = comm_peer_signal(L->comm, q) + R + me;
       }
-    SLLM_CUDA(launch_peer_signal(ready, j.epoch, s0));
-    comm_local_barrier(L->comm);  // in-process peers: every ready signal is queued before any wait
-    SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me), R, me, j.epoch, comm_timeout_ns(L->comm), j.d_err, s0));
+    const char* lost = "P2P fan-out: a peer rank of this process did not reach the fan-out within the timeout";
+    if (in_process) {
+      comm_record(L->comm, kPeerReady, s0);
+      if (!comm_local_barrier(L->comm)) fail(SLLM_E_PEER, lost);  // every ready event recorded before any wait
+      comm_wait_peers(L->comm, kPeerReady, s0);
+    } else {
+      SLLM_CUDA(launch_peer_signal(ready, j.epoch, s0));
+      SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me), R, me, j.epoch, comm_timeout_ns(L->comm), j.d_err, s0));
+    }
     j.fanout = pr.length - (j.hi - j.lo);
     if (cfg.verify && idx.block) {  // what arrived over NVLink is verified like what came over PCIe
       if (j.lo > 0) verify_range(idx, cfg, j, 0, j.lo, s0);
       if (j.hi < pr.length) verify_range(idx, cfg, j, j.hi, pr.length, s0);
     }
-    SLLM_CUDA(launch_peer_signal(done, j.epoch, s0));
-    comm_local_barrier(L->comm);  // ... and every done signal before the next load's done wait
-    if (R > 1) j.launches += 3;  // ready signal, ready wait, done signal
+    if (in_process) {
+      comm_record(L->comm, kPeerDone, s0);
+      if (!comm_local_barrier(L->comm)) fail(SLLM_E_PEER, lost);  // ... and every done event before the next load
+    } else {
+      SLLM_CUDA(launch_peer_signal(done, j.epoch, s0));
+      if (R > 1) j.launches += 3;  // ready signal, ready wait, done signal
+    }
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
     if (!P.plan.empty()) {  // SCATTER_CE from pinned DRAM: the window plan (every window fits a slot)

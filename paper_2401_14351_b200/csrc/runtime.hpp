@@ -116,6 +116,13 @@ uint32_t* comm_peer_signal(const sllm_comm* c, int q);
 uint64_t comm_timeout_ns(const sllm_comm* c);
 uint32_t comm_next_epoch(sllm_comm* c);
 uint8_t* comm_mc(const sllm_comm* c);  // NVLS: multicast address of replica byte 0 (else null)
+// In-process peer groups (every rank's handle lives in this process): stream ordering by
+// CUDA events, no device-side waits (fanout.cpp).
+enum PeerEvent { kPeerReady = 0, kPeerDone = 1 };
+bool comm_in_process(const sllm_comm* c);
+void comm_record(sllm_comm* c, PeerEvent which, cudaStream_t s);      // this rank's event, on s
+void comm_wait_peers(sllm_comm* c, PeerEvent which, cudaStream_t s);  // s waits on every peer's
+bool comm_local_barrier(sllm_comm* c);  // host rendezvous of the in-process ranks; false on timeout
 
 // ---- NVLS multicast group (nvls.cpp) -------------------------------------------------
 struct NvlsGroup;
@@ -124,7 +131,6 @@ size_t nvls_size(const NvlsGroup& g);
 uint8_t* nvls_mc(const NvlsGroup& g);
 uint8_t* nvls_replica(const NvlsGroup& g, int i);
 uint32_t* nvls_signal(const NvlsGroup& g, int i);
-void comm_local_barrier(sllm_comm* c);
 
 // GPUDirect Storage reads (gds.cpp): file bytes [lo, hi) -> dst + lo on `gpu`, `threads`
 // cuFile readers; landed(a, b) on the calling thread as the contiguous landed prefix grows.
@@ -141,7 +147,7 @@ inline void gran_table(const std::vector<Seg>& segs, uint64_t len, uint32_t shif
     while (s + 1 < segs.size() && segs[s + 1].off <= (g << shift)) ++s;
     out[g] = (uint32_t)s;
   }
-}  // host rendezvous of the group's in-process ranks
+}
 cudaStream_t comm_stream(sllm_comm* c, int s);
 
 }  // namespace sllm

