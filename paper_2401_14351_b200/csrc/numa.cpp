@@ -10,17 +10,27 @@
 #include <unistd.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "runtime.hpp"
 
 namespace sllm {
 
+// sysfs root ("/sys"; SLLM_SYSFS_ROOT points the host tests at a fake node tree)
+static const std::string& sysfs() {
+  static const std::string root = [] {
+    const char* e = getenv("SLLM_SYSFS_ROOT");
+    return std::string(e && *e ? e : "/sys");
+  }();
+  return root;
+}
+
 int numa_nodes() {
   static const int n = [] {
     int k = 0;
     for (int i = 0; i < 1024; ++i) {
-      std::string p = "/sys/devices/system/node/node" + std::to_string(i);
+      std::string p = sysfs() + "/devices/system/node/node" + std::to_string(i);
       if (access(p.c_str(), F_OK) != 0) break;
       ++k;
     }
@@ -38,7 +48,7 @@ int gpu_numa_node(int gpu) {
   std::string b(bus);
   for (auto& ch : b) ch = (char)tolower(ch);
   // cudaDeviceGetPCIBusId returns "0000:d1:00.0"; sysfs uses the same form
-  FILE* f = fopen(("/sys/bus/pci/devices/" + b + "/numa_node").c_str(), "r");
+  FILE* f = fopen((sysfs() + "/bus/pci/devices/" + b + "/numa_node").c_str(), "r");
   if (!f) return -1;
   int node = -1;
   if (fscanf(f, "%d", &node) != 1) node = -1;
@@ -72,7 +82,7 @@ bool parse_cpulist(const std::string& s, cpu_set_t* set) {
 }
 
 static bool node_cpus(int node, cpu_set_t* set) {
-  FILE* f = fopen(("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist").c_str(), "r");
+  FILE* f = fopen((sysfs() + "/devices/system/node/node" + std::to_string(node) + "/cpulist").c_str(), "r");
   if (!f) return false;
   char buf[4096] = {};
   const size_t n = fread(buf, 1, sizeof buf - 1, f);
@@ -80,15 +90,20 @@ static bool node_cpus(int node, cpu_set_t* set) {
   return parse_cpulist(std::string(buf, n), set);
 }
 
-// Pin the calling thread to the CPUs of `node` (intersected with the process's allowed
-// set).  Returns true if the affinity changed.
+// Pin the calling thread to the CPUs of `node`, intersected with the process's allowed set
+// -- the main thread's mask, not the calling thread's: a pooled load worker bound to one
+// node for one job is re-bound to another node for the next (its own mask would intersect
+// to nothing).  An unknown node, or one with no allowed CPU, unbinds the thread (process
+// mask).  Returns true if the affinity was set.
 bool bind_thread_to_node(int node) {
-  if (node < 0 || numa_nodes() <= 1) return false;
+  if (numa_nodes() <= 1) return false;
   cpu_set_t want, allowed, both;
-  if (!node_cpus(node, &want)) return false;
-  if (sched_getaffinity(0, sizeof allowed, &allowed) != 0) return false;
-  CPU_AND(&both, &want, &allowed);
-  if (CPU_COUNT(&both) == 0) return false;
+  if (sched_getaffinity(getpid(), sizeof allowed, &allowed) != 0) return false;
+  both = allowed;
+  if (node >= 0 && node_cpus(node, &want)) {
+    CPU_AND(&both, &want, &allowed);
+    if (CPU_COUNT(&both) == 0) both = allowed;
+  }
   return sched_setaffinity(0, sizeof both, &both) == 0;
 }
 

@@ -74,3 +74,26 @@ def test_pinned_pages_on_the_gpus_node_and_caller_affinity_kept():
     res = sllm.load(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20))      # node-bound worker
     res.wait()
     assert os.sched_getaffinity(0) == before         # the library never re-binds the caller
+
+
+def test_worker_rebinds_across_nodes_fake_sysfs(tmp_path):
+    """A pooled worker bound to one node for one job is re-bound to another node for the
+    next, and unbound for an unknown node (numa.cpp against a fake two-node sysfs tree)."""
+    import subprocess
+    cpus = sorted(os.sched_getaffinity(0))
+    if len(cpus) < 2:
+        pytest.skip("needs two allowed CPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for n, c in enumerate(cpus[:2]):
+        d = tmp_path / "devices" / "system" / "node" / f"node{n}"
+        d.mkdir(parents=True)
+        (d / "cpulist").write_text(f"{c}\n")
+    exe = str(tmp_path / "numa_bind")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-o", exe, os.path.join(root, "tests", "c", "numa_bind.cpp"),
+                        f"-I{root}/include", f"-I{cuda}/include", f"-L{cuda}/lib64", "-lcudart_static",
+                        "-lpthread", "-ldl", "-lrt"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-4000:]
+    r = subprocess.run([exe, str(cpus[0]), str(cpus[1])], capture_output=True, text=True, timeout=60,
+                       env={**os.environ, "SLLM_SYSFS_ROOT": str(tmp_path)})
+    assert r.returncode == 0 and "numa bind ok" in r.stdout, r.stdout + r.stderr
