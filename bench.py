@@ -964,6 +964,9 @@ def main(argv=None):
                 ("checksum only" if args.mode == "ce" else "scatter+checksum"),
                 "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
                 "bytes_per_launch": per_launch_bytes,
+                "peak_what": "MEASURED_PEAKS.json hbm_gbs: a device copy's read+write bytes per second; K4 only "
+                             "reads, and a read-only stream has no read/write turnaround on the HBM bus, so it can "
+                             "exceed the copy figure (ncu: K4 at ~90 % of the DRAM peak, profiles/r02)",
                 "note": "two CTAs per SM, units handed out by ticket; each launch verifies a span of landed windows "
                         "(up to 4 GiB, shrinking towards the end) beside the PCIe copies"}
         span_ms = sum(r.get("t_kernel_span_ms_sum", 0.0) for r in reports) / len(reports)

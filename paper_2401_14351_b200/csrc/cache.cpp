@@ -78,10 +78,18 @@ void cache_acquire(sllm_cache* c, const char* dir, int io_threads, const sllm_in
                    int32_t* hit) {
   if (!c || !dir || !index || !bufs) fail(SLLM_E_INVALID, "null argument");
   const std::string key(dir);
+  std::unique_ptr<sllm_index> parsed;  // a miss's index, read and parsed outside the lock
   std::unique_lock<std::mutex> g(c->mu);
   for (;;) {
     auto it = c->models.find(key);
-    if (it == c->models.end()) break;
+    if (it == c->models.end()) {
+      if (parsed) break;
+      g.unlock();  // storage read + parse: hits on other models are not held up by it
+      std::vector<uint8_t> blob = read_file((key + "/index.bin").c_str());
+      parsed.reset(parse(blob.data(), blob.size()));
+      g.lock();
+      continue;  // look again: another acquirer may have started this model meanwhile
+    }
     if (!it->second.ready) {  // another thread is reading it: wait, then look again
       c->cv.wait(g);
       continue;
@@ -94,9 +102,8 @@ void cache_acquire(sllm_cache* c, const char* dir, int io_threads, const sllm_in
     if (hit) *hit = 1;
     return;
   }
-  // miss: parse the index, reserve the bytes (evicting unheld models, LRU first)
-  std::vector<uint8_t> blob = read_file((key + "/index.bin").c_str());
-  sllm_index* idx = parse(blob.data(), blob.size());
+  // miss: reserve the bytes (evicting unheld models, LRU first)
+  sllm_index* idx = parsed.release();
   uint64_t need = 0;
   for (auto& pr : idx->parts) need += align_up(pr.length, 2ull << 20);
   if (need > c->capacity) {
