@@ -781,9 +781,10 @@ def main(argv=None):
         import torch.distributed as dist
         if not SAME_GPU and visible_gpus() < world:
             fail_loudly(f"{world} ranks need {world} visible GPUs, found {visible_gpus()}")
-        if SAME_GPU and args.fanout == "p2p":  # ranks as processes wait on each other's device-side flags
-            fail_loudly("--fanout p2p with one process per rank needs one GPU per rank (its kernels wait on "
-                        "the peers' flags); SLLM_BENCH_SAME_GPU covers the sharded and NCCL paths only")
+        if SAME_GPU and args.fanout == "p2p":
+            # ranks sharing a GPU must not run kernels that spin on each other's flags: the
+            # load workers wait for the peers' flags on the host instead
+            os.environ["SLLM_PEER_WAIT"] = "host"
         torch.cuda.set_device(gpu_of(local))
         if SAME_GPU:
             dist.init_process_group("gloo")
@@ -1030,7 +1031,9 @@ def main(argv=None):
                 "config": arm_config(args, config, world, len(parts), payload_bytes, raw_bytes, replicated, {
                     **({"spread": f"{len(parts)} partitions over GPUs {used} from one process"} if args.spread else {}),
                     **({"same_gpu_plumbing_check": "all ranks on cuda:0 (gloo); not a scaling number"}
-                       if SAME_GPU and world > 1 else {})}),
+                       if SAME_GPU and world > 1 else {}),
+                    **({"peer_wait": "host (load workers poll the peers' flags; no kernel waits on another rank)"}
+                       if os.environ.get("SLLM_PEER_WAIT") == "host" and args.fanout == "p2p" else {})}),
                 "time_to_loaded_model_s": ms_step * 1e-3, "step_ms": step_stats(ms_steps),
                 "t_alloc_s": t_alloc, "t_setup_s": t_setup,
                 "b_h2d_measured_GBps": b_h2d, "frac_h2d": pcie_rate / b_h2d,

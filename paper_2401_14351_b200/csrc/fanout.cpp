@@ -102,7 +102,8 @@ struct sllm_comm {
   std::vector<uint32_t*> signal;
   uint32_t epoch = 0;
   uint64_t timeout_ns = 0;
-  cudaStream_t streams[sllm::kMaxStreams + 1] = {};
+  cudaStream_t streams[sllm::kMaxStreams + 2] = {};  // transfer, kernel, host-wait poll
+  uint32_t* poll = nullptr;                            // pinned copy of the own signal words (host wait)
   std::shared_ptr<sllm::LocalGroup> local;  // the in-process ranks of this peer group
   cudaEvent_t ev[2] = {};                    // this rank's ready / done events (in-process groups)
   // NVLS group (SLLM_FANOUT_NVLS): the multicast object and the library-owned replicas it
@@ -181,7 +182,40 @@ static void join_local_events(sllm_comm* c) {
   for (int w = 0; w < 2; ++w) c->local->ev[w][c->rank] = c->ev[w];
 }
 
-cudaStream_t comm_stream(sllm_comm* c, int s) {  // s = 0..kMaxStreams-1 transfer, kMaxStreams = kernel
+// SLLM_PEER_WAIT=host: a one-process-per-rank group waits for its peers' flags on the host
+// (the load's worker thread polls its own signal words with a small device->host copy)
+// instead of with a device-side wait kernel.  No kernel then waits for another process's
+// kernel, so the ranks may share a GPU (the multi-process wiring tested on one GPU); the
+// flags themselves are written as in the default mode (peer_signal_kernel).
+bool comm_host_wait() {
+  static const bool host = [] {
+    const char* e = getenv("SLLM_PEER_WAIT");
+    return e && std::string(e) == "host";
+  }();
+  return host;
+}
+
+void comm_wait_flags_host(sllm_comm* c, const uint32_t* own, uint32_t epoch) {
+  if (c->nranks <= 1) return;
+  if (!c->poll) SLLM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->poll), 4 * (size_t)c->nranks, cudaHostAllocDefault));
+  cudaStream_t s = comm_stream(c, kMaxStreams + 1);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    SLLM_CUDA(cudaMemcpyAsync(c->poll, own, 4 * (size_t)c->nranks, cudaMemcpyDeviceToHost, s));
+    SLLM_CUDA(cudaStreamSynchronize(s));
+    int missing = -1;
+    for (int q = 0; q < c->nranks && missing < 0; ++q)
+      if (q != c->rank && (int32_t)(c->poll[q] - epoch) < 0) missing = q;
+    if (missing < 0) return;
+    if ((uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count() >
+        c->timeout_ns)
+      fail(SLLM_E_PEER, "P2P fan-out: peer rank " + std::to_string(missing) +
+                            " did not signal completion within the timeout (host wait)");
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+cudaStream_t comm_stream(sllm_comm* c, int s) {  // s = 0..kMaxStreams-1 transfer, kMaxStreams kernel, +1 poll
   if (!c->streams[s]) SLLM_CUDA(cudaStreamCreateWithFlags(&c->streams[s], cudaStreamNonBlocking));
   return c->streams[s];
 }
@@ -368,6 +402,7 @@ void sllm_comm_free_internal(sllm_comm* c) {
       }
     for (auto& e : c->ev)
       if (e) cudaEventDestroy(e);
+    if (c->poll) cudaFreeHost(c->poll);
   }
   delete c;
 }

@@ -618,6 +618,8 @@ static void run_job(sllm_load* L, PartJob& j) {
     const int R = comm_nranks(L->comm), me = comm_rank(L->comm);
     if (in_process) {
       comm_wait_peers(L->comm, kPeerDone, s0);
+    } else if (comm_host_wait()) {
+      comm_wait_flags_host(L->comm, comm_peer_signal(L->comm, me) + R, j.epoch - 1);
     } else {
       SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me) + R, R, me, j.epoch - 1, comm_timeout_ns(L->comm),
                                  j.d_err, s0));
@@ -741,7 +743,12 @@ static void run_job(sllm_load* L, PartJob& j) {
       comm_wait_peers(L->comm, kPeerReady, s0);
     } else {
       SLLM_CUDA(launch_peer_signal(ready, j.epoch, s0));
-      SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me), R, me, j.epoch, comm_timeout_ns(L->comm), j.d_err, s0));
+      if (comm_host_wait()) {
+        comm_wait_flags_host(L->comm, comm_peer_signal(L->comm, me), j.epoch);
+        if (R > 1) j.launches--;  // (no wait kernel)
+      } else {
+        SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me), R, me, j.epoch, comm_timeout_ns(L->comm), j.d_err, s0));
+      }
     }
     j.fanout = pr.length - (j.hi - j.lo);
     if (cfg.verify && idx.block) {  // what arrived over NVLink is verified like what came over PCIe

@@ -123,6 +123,9 @@ bool comm_in_process(const sllm_comm* c);
 void comm_record(sllm_comm* c, PeerEvent which, cudaStream_t s);      // this rank's event, on s
 void comm_wait_peers(sllm_comm* c, PeerEvent which, cudaStream_t s);  // s waits on every peer's
 bool comm_local_barrier(sllm_comm* c);  // host rendezvous of the in-process ranks; false on timeout
+bool comm_host_wait();                  // SLLM_PEER_WAIT=host: multi-process peers waited for on the host
+// host wait until own[q] >= epoch for every peer q (SLLM_E_PEER after the group timeout)
+void comm_wait_flags_host(sllm_comm* c, const uint32_t* own, uint32_t epoch);
 
 // ---- NVLS multicast group (nvls.cpp) -------------------------------------------------
 struct NvlsGroup;

@@ -6,8 +6,10 @@ device-side release/acquire signals order the peers' stores before each rank ver
 what it received.  Only one GPU is available here, so the "peers" are R replicas on the
 same GPU in one process (plain pointers; the in-process ranks order each other with CUDA
 events, so no kernel waits for another rank's kernel).  The one-process-per-rank wiring
-(CUDA IPC handles exchanged over a gloo group, device-side flag waits) needs one GPU per
-rank: kernels that spin on another rank's flag must not share a GPU.  Every replica must equal the oracle's partition P_0
+(CUDA IPC handles exchanged over a gloo group, flags written by the peers' kernels) runs on
+one GPU with the flags waited for on the host (SLLM_PEER_WAIT=host); its device-side wait
+kernels need one GPU per rank -- kernels that spin on another rank's flag must not share a
+GPU.  Every replica must equal the oracle's partition P_0
 byte for byte (O9(c)) and every block checksum must equal the oracle's (O9(d)).
 """
 import os
@@ -157,12 +159,12 @@ def _free_port():
     return port
 
 
-def _ipc_worker(rank, world, port, mode, q):
+def _ipc_worker(rank, world, port, mode, wait, q):
     try:
         import torch.distributed as dist
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SLLM_PEER_WAIT=wait)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        torch.cuda.set_device(rank)
+        torch.cuda.set_device(rank if wait == "device" else 0)
         inv, seed = models.model_inventory("toy")
         idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
         lay, oparts, _ = oracle_of(inv, seed)
@@ -190,17 +192,19 @@ def _ipc_worker(rank, world, port, mode, q):
         q.put((rank, False, repr(ex)))
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="one process per rank spins on device-side flags: "
-                    "needs one GPU per rank")
+@pytest.mark.parametrize("wait", ["host", "device"])
 @pytest.mark.parametrize("mode", ["ce", "zerocopy"])
-def test_p2p_fanout_two_processes_ipc(mode):
-    """Two processes, one replica each on its own GPU, peers mapped with CUDA IPC (the real
-    multi-process wiring of bench.py --fanout p2p)."""
+def test_p2p_fanout_two_processes_ipc(mode, wait):
+    """Two processes, one replica each, peers mapped with CUDA IPC (the real multi-process
+    wiring of bench.py --fanout p2p).  wait=host: both ranks on GPU 0, flags polled by the
+    load workers; wait=device: the device-side wait kernels, one GPU per rank."""
+    if wait == "device" and torch.cuda.device_count() < 2:
+        pytest.skip("device-side flag waits of one process per rank need one GPU per rank")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, mode, wait, q)) for r in range(2)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in procs]

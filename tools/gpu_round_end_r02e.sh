@@ -25,9 +25,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:mate
 # (compute-sanitizer is closed on the GPU pool from this session on; earlier clean logs: profiles/r02/final4/sanitizer)
 timeout 600 python tools/probe_p2p_group.py > $O/probe_p2p_group.log 2>&1; echo rc=$? >> $O/probe_p2p_group.log
 ls -la $O > $O/ls.txt
-# 2-rank plumbing on the one GPU (torchrun, gloo): sharded line (multi-process P2P needs one GPU per rank)
+# 2-rank plumbing on the one GPU (torchrun, gloo): sharded and P2P-fan-out lines (the P2P ranks wait for each
+# other's flags on the host: SLLM_PEER_WAIT=host, set by bench.py under SLLM_BENCH_SAME_GPU)
 SLLM_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
     bench.py --gpus 2 --config opt-6.7b --steps 3 --warmup 3 --no-cpu-baseline --no-standalone > $O/bench_n2_samegpu_none.json 2> $O/bench_n2_samegpu_none.err
+SLLM_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 \
+    bench.py --gpus 2 --config opt-6.7b --fanout p2p --steps 3 --warmup 3 --no-cpu-baseline --no-standalone > $O/bench_n2_samegpu_p2p.json 2> $O/bench_n2_samegpu_p2p.err
 # 4 and 8 ranks on the one GPU (plumbing of the N > 1 bench path: barriers, B_h2d(N), max over ranks)
 SLLM_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29535 \
     bench.py --gpus 4 --config opt-6.7b --steps 2 --warmup 3 --no-cpu-baseline --no-standalone > $O/bench_n4_samegpu_none.json 2> $O/bench_n4_samegpu_none.err
