@@ -359,9 +359,14 @@ SLLM_API sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_com
  *   timeout_ms    : how long a rank waits for its peers' completion signals before the
  *                   load fails with SLLM_E_PEER (0 = 60000).
  * A P2P load completes only when every rank's load has run.  Ranks of one group that share
- * a process rendezvous on the host around their peer signals (so no rank's device-side wait
- * can block a peer's work queued behind it), and their caller streams are ordered after
- * the load in sllm_load_wait, not in sllm_load_start.
+ * a process order each other with CUDA events (no signal words, no device-side waits; they
+ * rendezvous on the host so every event is recorded before it is waited on, and a rank that
+ * never arrives fails the others with SLLM_E_PEER after timeout_ms), and their caller
+ * streams are ordered after the load in sllm_load_wait, not in sllm_load_start.  Ranks in
+ * separate processes wait for each other's signal words with a device-side wait kernel, or,
+ * with the environment variable SLLM_PEER_WAIT=host, on the host (the load's worker polls its
+ * own signal words) -- required when the ranks share a GPU: a kernel spinning on another
+ * process's flag must not share a GPU with the kernel that sets it.
  * The handle owns its streams; sllm_comm_free releases them (never the replicas). */
 SLLM_API sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
                                           uint32_t* const* peer_signal, uint64_t timeout_ms, sllm_comm** out);
