@@ -216,6 +216,36 @@ def peaks():
         return {}
 
 
+def bitexact_sample(res, inv, seed: int, torch, n_random: int = 10) -> dict:
+    """Sampled tensors of a finished load compared byte for byte with the seeded payload
+    generator (synth/payload.py, the inputs' own source -- no oracle arithmetic): the first
+    and last three tensors in source order, the largest, the smallest and `n_random` seeded
+    picks.  Every block of every timed load was also checked on the GPU against the index's
+    Fletcher-64 table (a mismatch fails the load with SLLM_E_CHECKSUM)."""
+    import random
+    import numpy as np
+    from synth import payload
+    cand = [e for e, t in enumerate(inv) if t.name in res.tensors]
+    if not cand:
+        return None
+    pick = set(cand[:3] + cand[-3:])
+    pick.add(max(cand, key=lambda e: inv[e].nbytes))
+    pick.add(min(cand, key=lambda e: inv[e].nbytes))
+    pick.update(random.Random(seed).sample(cand, min(n_random, len(cand))))
+    pick = sorted(pick)
+    want = [np.empty(inv[e].nbytes, np.uint8) for e in pick]
+    payload.payload_into([a.ctypes.data for a in want], [a.size for a in want], seed, pick)
+    equal = True
+    for e, w in zip(pick, want):
+        got = res.tensors[inv[e].name].reshape(-1).view(torch.uint8).cpu().numpy()
+        equal &= bool(np.array_equal(got, w))
+    return {"equal": equal, "tensors_checked": len(pick), "tensors_loaded": len(cand),
+            "bytes_checked": int(sum(inv[e].nbytes for e in pick)),
+            "against": "seeded payload generator (synth/payload.py), last timed load, untimed",
+            "every_block_checked_on_gpu": "each timed load compared every 1 MiB block's Fletcher-64 with the "
+                                          "index table (mismatch = SLLM_E_CHECKSUM)"}
+
+
 def host_description() -> dict:
     """the host cores the oracle runs on."""
     model = None
@@ -894,7 +924,9 @@ def main(argv=None):
             prev = (res, ix)
             del res, ix
         sync_all()
-        prev = None
+    # the last timed load's tensors vs the seeded payloads, byte for byte (untimed)
+    bitexact = bitexact_sample(prev[0], inv, seed, torch) if prev is not None else None
+    prev = None
     gc.unfreeze()
     if world > 1:
         dist.barrier()
@@ -1034,7 +1066,7 @@ def main(argv=None):
                        if SAME_GPU and world > 1 else {}),
                     **({"peer_wait": "host (load workers poll the peers' flags; no kernel waits on another rank)"}
                        if os.environ.get("SLLM_PEER_WAIT") == "host" and args.fanout == "p2p" else {})}),
-                "time_to_loaded_model_s": ms_step * 1e-3, "step_ms": step_stats(ms_steps),
+                "time_to_loaded_model_s": ms_step * 1e-3, "step_ms": step_stats(ms_steps), "bitexact": bitexact,
                 "t_alloc_s": t_alloc, "t_setup_s": t_setup,
                 "b_h2d_measured_GBps": b_h2d, "frac_h2d": pcie_rate / b_h2d,
                 "gpu_launches": int(rep["kernel_launches"]) * args.steps,
