@@ -743,6 +743,9 @@ static void run_job(sllm_load* L, PartJob& j) {
       comm_wait_peers(L->comm, kPeerReady, s0);
     } else {
       SLLM_CUDA(launch_peer_signal(ready, j.epoch, s0));
+      // (a group split over processes with several ranks in this one: those ranks still queue
+      // every ready signal before any wait, so no wait sits ahead of a peer's signal)
+      comm_local_barrier(L->comm);
       if (comm_host_wait()) {
         comm_wait_flags_host(L->comm, comm_peer_signal(L->comm, me), j.epoch);
         if (R > 1) j.launches--;  // (no wait kernel)
@@ -760,6 +763,7 @@ static void run_job(sllm_load* L, PartJob& j) {
       if (!comm_local_barrier(L->comm)) fail(SLLM_E_PEER, lost);  // ... and every done event before the next load
     } else {
       SLLM_CUDA(launch_peer_signal(done, j.epoch, s0));
+      comm_local_barrier(L->comm);  // (same: every done signal before the next load's done wait)
       if (R > 1) j.launches += 3;  // ready signal, ready wait, done signal
     }
   } else {
