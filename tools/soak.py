@@ -2,6 +2,7 @@
 free each time, rotating modes), watching device free memory and host RSS for leaks.
 
     python tools/soak.py [--config opt-6.7b] [--loads 100]
+    python tools/soak.py --config lora-70b-r32 --loads 300 --p2p 2   # in-process P2P group
 
 Prints one JSON line: loads, failures, seconds, device free memory and RSS before / after
 (after the library's idle cache is trimmed), and the GB/s range."""
@@ -25,6 +26,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="opt-6.7b")
     ap.add_argument("--loads", type=int, default=100)
+    ap.add_argument("--p2p", type=int, default=0, help="R > 1: an in-process P2P group of R replicas on GPU 0 "
+                    "(event-ordered), every load verified on every replica")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -35,6 +38,8 @@ def main():
     inv, seed = models.model_inventory(args.config)
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=[0], gpu_of={0: 0})
     table = idx.block_checksums(0)
+    if args.p2p > 1:
+        return soak_p2p(args, sllm, torch, np, idx, bufs, table)
     modes = ["ce", "zerocopy", "scatter_ce", "scatter_zc", "auto"]
     # warm once per mode (pools, module load), then measure the baseline
     for m in modes:
@@ -67,6 +72,42 @@ def main():
                       "maxrss_GB": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6,
                       "per_mode_GBps": {m: {"min": min(v), "median": float(np.median(v)), "slowest_load": int(np.argmin(v))}
                                         for m, v in by_mode.items() if v}}), flush=True)
+
+
+def soak_p2p(args, sllm, torch, np, idx, bufs, table):
+    """Back-to-back loads of one in-process P2P group (R replicas on GPU 0, CUDA-event
+    ordering, one epoch per load), rotating CE / zero-copy; every replica's block checksums
+    must equal the index table after every load."""
+    R, L = args.p2p, idx.partitions[0].length
+    bases = [torch.empty(L, dtype=torch.uint8, device="cuda") for _ in range(R)]
+    sigs = [torch.zeros(2 * R, dtype=torch.int32, device="cuda") for _ in range(R)]
+    comms = [sllm.Comm.peers(R, r, 0, [b.data_ptr() for b in bases], [s.data_ptr() for s in sigs], 60000)
+             for r in range(R)]
+    modes = ["ce", "zerocopy"]
+    torch.cuda.synchronize()
+    free0, rss0 = torch.cuda.mem_get_info(0)[0], rss_gb()
+    rates, failures = [], 0
+    t0 = time.perf_counter()
+    for i in range(args.loads):
+        cfg = sllm.LoadConfig(chunk_bytes=64 << 20, mode=modes[i % 2], fanout="p2p")
+        ts = time.perf_counter()
+        rs = [sllm.load_start(idx, bufs, {0: 0}, cfg, {0: bases[r]}, None, None, comms[r]) for r in range(R)]
+        for r in rs:
+            r.wait()
+        rates.append(R * L / (time.perf_counter() - ts) / 1e9)
+        failures += sum(not np.array_equal(r.block_checksums(0), table) for r in rs)
+        del rs
+    dt = time.perf_counter() - t0
+    equal = all(torch.equal(bases[0], b) for b in bases[1:])
+    for c in comms:
+        c.free()
+    torch.cuda.synchronize()
+    free1, rss1 = torch.cuda.mem_get_info(0)[0], rss_gb()
+    print(json.dumps({"config": args.config, "p2p_ranks": R, "loads": args.loads, "failures": failures,
+                      "replicas_equal": equal, "seconds": dt, "GBps_replicas_min": min(rates),
+                      "GBps_replicas_median": float(np.median(rates)), "device_free_GB_before": free0 / 1e9,
+                      "device_free_GB_after": free1 / 1e9, "device_leak_GB": (free0 - free1) / 1e9,
+                      "rss_GB_before": rss0, "rss_GB_after": rss1}), flush=True)
 
 
 if __name__ == "__main__":
