@@ -84,7 +84,13 @@ def soak_p2p(args, sllm, torch, np, idx, bufs, table):
     comms = [sllm.Comm.peers(R, r, 0, [b.data_ptr() for b in bases], [s.data_ptr() for s in sigs], 60000)
              for r in range(R)]
     modes = ["ce", "zerocopy"]
+    for m in modes:  # warm once per mode (worker threads, pools), then measure the baseline
+        cfg = sllm.LoadConfig(chunk_bytes=64 << 20, mode=m, fanout="p2p")
+        for r in [sllm.load_start(idx, bufs, {0: 0}, cfg, {0: bases[r]}, None, None, comms[r]) for r in range(R)]:
+            r.wait()
     torch.cuda.synchronize()
+    sllm.trim_device_cache(0)
+    torch.cuda.empty_cache()
     free0, rss0 = torch.cuda.mem_get_info(0)[0], rss_gb()
     rates, failures = [], 0
     t0 = time.perf_counter()
@@ -98,11 +104,13 @@ def soak_p2p(args, sllm, torch, np, idx, bufs, table):
         failures += sum(not np.array_equal(r.block_checksums(0), table) for r in rs)
         del rs
     dt = time.perf_counter() - t0
-    equal = all(torch.equal(bases[0], b) for b in bases[1:])
+    torch.cuda.synchronize()
+    sllm.trim_device_cache(0)
+    torch.cuda.empty_cache()
+    free1, rss1 = torch.cuda.mem_get_info(0)[0], rss_gb()
+    equal = all(torch.equal(bases[0], b) for b in bases[1:])  # (its temporaries come after the reading)
     for c in comms:
         c.free()
-    torch.cuda.synchronize()
-    free1, rss1 = torch.cuda.mem_get_info(0)[0], rss_gb()
     print(json.dumps({"config": args.config, "p2p_ranks": R, "loads": args.loads, "failures": failures,
                       "replicas_equal": equal, "seconds": dt, "GBps_replicas_min": min(rates),
                       "GBps_replicas_median": float(np.median(rates)), "device_free_GB_before": free0 / 1e9,
