@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--clocks", type=int, default=1)
     ap.add_argument("--gc", type=int, default=1, help="0: gc.disable() during the loop; 2: gc.freeze() first")
     ap.add_argument("--overlap-free", type=int, default=0, help="1: drop the previous load's handles during the next")
+    ap.add_argument("--verify", type=int, default=1)
+    ap.add_argument("--streams", type=int, default=2)
     args = ap.parse_args()
     import torch
     import bench
@@ -34,7 +36,8 @@ def main():
     inv, seed = models.model_inventory(args.config)
     idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20, args.config, partitions=[0], gpu_of={0: 0})
     blob = idx.serialize()
-    cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, mode=args.mode, profile=bool(args.profile))
+    cfg = sllm.LoadConfig(chunk_bytes=args.chunk_mib << 20, mode=args.mode, profile=int(args.profile),
+                          verify=bool(args.verify), n_streams=args.streams)
     bases, per = sllm.allocate(idx, {0: 0}, cfg.scatter)
     st = torch.cuda.current_stream()
     rows = []
