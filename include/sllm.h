@@ -365,8 +365,9 @@ SLLM_API sllm_status sllm_comm_init_all(const int32_t* gpus, int32_t n, sllm_com
  * streams are ordered after the load in sllm_load_wait, not in sllm_load_start.  Ranks in
  * separate processes wait for each other's signal words with a device-side wait kernel, or,
  * with the environment variable SLLM_PEER_WAIT=host, on the host (the load's worker polls its
- * own signal words) -- required when the ranks share a GPU: a kernel spinning on another
- * process's flag must not share a GPU with the kernel that sets it.
+ * own signal words; the caller's stream is then ordered after the load in sllm_load_wait)
+ * -- required when the ranks share a GPU: a kernel spinning on another process's flag must
+ * not share a GPU with the kernel that sets it.
  * The handle owns its streams; sllm_comm_free releases them (never the replicas). */
 SLLM_API sllm_status sllm_comm_init_peers(int32_t nranks, int32_t rank, int32_t gpu, void* const* peer_base,
                                           uint32_t* const* peer_signal, uint64_t timeout_ms, sllm_comm** out);

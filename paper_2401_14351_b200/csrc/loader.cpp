@@ -748,7 +748,6 @@ static void run_job(sllm_load* L, PartJob& j) {
       comm_local_barrier(L->comm);
       if (comm_host_wait()) {
         comm_wait_flags_host(L->comm, comm_peer_signal(L->comm, me), j.epoch);
-        if (R > 1) j.launches--;  // (no wait kernel)
       } else {
         SLLM_CUDA(launch_peer_wait(comm_peer_signal(L->comm, me), R, me, j.epoch, comm_timeout_ns(L->comm), j.d_err, s0));
       }
@@ -764,7 +763,7 @@ static void run_job(sllm_load* L, PartJob& j) {
     } else {
       SLLM_CUDA(launch_peer_signal(done, j.epoch, s0));
       comm_local_barrier(L->comm);  // (same: every done signal before the next load's done wait)
-      if (R > 1) j.launches += 3;  // ready signal, ready wait, done signal
+      if (R > 1) j.launches += comm_host_wait() ? 2 : 3;  // ready signal, [ready wait,] done signal
     }
   } else {
     const uint64_t nch = ceil_div(pr.length, C);
@@ -1121,7 +1120,9 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
       for (auto& e : j.ev) SLLM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
       if (j.origin) {
         SLLM_CUDA(cudaEventRecord(j.ev[3], j.origin));
-        j.eager = j.file.empty() && !(group_fanout && comm_local_members(comm) > 1);
+        // (a group whose issue waits for its peers -- in-process ranks, host-polled flags --
+        // orders the caller's stream in sllm_load_wait, so sllm_load_start stays asynchronous)
+        j.eager = j.file.empty() && !(group_fanout && (comm_local_members(comm) > 1 || comm_host_wait()));
       }
     }
   } catch (...) {
