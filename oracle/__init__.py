@@ -1,7 +1,9 @@
 """CPU ORACLE for the loading-optimized checkpoint path -- TEST INFRASTRUCTURE ONLY.
 
-Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
-``--impl reference`` legs may import this package.  The product (the C-ABI library
+Only ``tests/`` (incl. the compute-sanitizer harness ``tests/sanitize_gpu.py``),
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs
+may import this package (and ``tools/bench_convert.py``, which times the oracle converter as
+the converter benchmark's CPU baseline -- the cpu_baseline role).  The product (the C-ABI library
 ``paper_2401_14351_b200/libsllm.so`` and its Python binding) never imports, links or
 executes anything here, and nothing here imports the product: the two share no code,
 no headers, no constants and no helpers.  The only shared module is ``synth/``

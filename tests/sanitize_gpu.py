@@ -1,7 +1,7 @@
 """Small loads in every mode / engine / fan-out for compute-sanitizer (memcheck, racecheck,
 synccheck, initcheck), each checked byte-exact against the CPU oracle:
 
-    compute-sanitizer --tool memcheck --error-exitcode 99 python tools/sanitize_gpu.py
+    compute-sanitizer --tool memcheck --error-exitcode 99 python tests/sanitize_gpu.py
 """
 import os
 import sys
