@@ -71,6 +71,9 @@ def test_p2p_fanout_same_gpu(R, mode, chunk):
             lo, hi = slices[r]
             assert rep["transferred_bytes"] == hi - lo          # each byte crosses "PCIe" once
             assert rep["fanout_bytes"] == L - (hi - lo)
+            # in-process ranks are ordered by CUDA events: the slice's one loading launch
+            # (a toy slice is one copy window) + K4 on each received range, no signal / wait kernels
+            assert rep["kernel_launches"] == (1 if hi > lo else 0) + (lo > 0) + (hi < L), rep["kernel_launches"]
             for e in (0, len(inv) - 2, len(inv) - 1):           # views of this replica
                 t = inv[e]
                 got = res.tensors[t.name].reshape(-1).view(torch.uint8).cpu().numpy()
