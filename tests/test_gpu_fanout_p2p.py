@@ -195,6 +195,54 @@ def _ipc_worker(rank, world, port, mode, wait, q):
         q.put((rank, False, repr(ex)))
 
 
+def _ipc_absent_peer_worker(rank, world, port, q):
+    """Rank 1 joins the group but never loads: rank 0's host-polled wait must fail with
+    SLLM_E_PEER after the group timeout (and not hang)."""
+    try:
+        import time
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SLLM_PEER_WAIT="host")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        inv, seed = models.model_inventory("toy")
+        idx, bufs = workloads.build_pinned(inv, seed, 4096, 1 << 20)
+        base = torch.empty(idx.partitions[0].length, dtype=torch.uint8, device="cuda")
+        comm = sllm.Comm.peers_from_process_group(base, timeout_ms=1500)
+        ok, msg = True, ""
+        if rank == 0:
+            t0 = time.perf_counter()
+            res = sllm.load_start(idx, bufs, {0: 0}, sllm.LoadConfig(chunk_bytes=1 << 20, mode="ce", fanout="p2p"),
+                                  {0: base}, None, None, comm)
+            try:
+                res.wait()
+                ok, msg = False, "load succeeded without its peer"
+            except sllm.SllmError as ex:
+                dt = time.perf_counter() - t0
+                ok = ex.status == 12 and 1.0 < dt < 30.0
+                msg = f"status {ex.status} after {dt:.2f} s: {ex}"
+            del res
+        dist.barrier()  # rank 1 keeps its replica mapped until rank 0 is done
+        comm.free()
+        dist.destroy_process_group()
+        q.put((rank, ok, msg))
+    except Exception as ex:  # noqa: BLE001
+        q.put((rank, False, repr(ex)))
+
+
+def test_p2p_two_processes_absent_peer_host_wait_times_out():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_absent_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in out), out
+
+
 @pytest.mark.parametrize("wait", ["host", "device"])
 @pytest.mark.parametrize("mode", ["ce", "zerocopy"])
 def test_p2p_fanout_two_processes_ipc(mode, wait):
