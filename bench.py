@@ -991,8 +991,10 @@ def main(argv=None):
         achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9
         hbm = peaks().get("hbm_gbs", 6551.4)
         traffic, traffic_src = ncu_traffic(args.mode, per_launch_bytes)
+        dram_pct, _ = ncu_traffic(args.mode, 1.0, key="dram_pct_of_peak")
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "traffic_source": traffic_src,
+                "ncu_dram_pct_of_peak": dram_pct,  # the captured launch against ncu's own DRAM peak (cold)
                 "kernel": "materialise_tma_kernel<%s> (in pipeline)" %
                 ("checksum only" if args.mode == "ce" else "scatter+checksum"),
                 "launches_per_step": kern_launches, "avg_launch_ms": avg_ms,
