@@ -646,7 +646,7 @@ def standalone_hbm(idx, bufs, torch, sllm, reps=5):
     res["k4"] = {"bytes": n, "ms": t * 1e3, "GBps": n / t / 1e9,
                  "checksums_equal_index": bool((out.cpu().numpy().view("uint64") == table).all())}
     # K3: scatter the whole partition image into per-tensor buffers (read L + write payload)
-    _, per = sllm.allocate(idx, {p: 0}, scatter=True, partitions=[p])
+    _, per = sllm.allocate(idx, {p: torch.cuda.current_device()}, scatter=True, partitions=[p])  # beside `src`
     ts = [sllm.materialise_device(idx, p, src.data_ptr(), per, 0, st, timed=True) for _ in range(reps)]
     t = min(ts) * 1e-3
     payload = sum(x.nbytes for x in idx.tensors if x.partition == p)
