@@ -81,6 +81,10 @@ def parse(argv=None):
     ap.add_argument("--no-standalone", action="store_true")
     ap.add_argument("--no-baselines", action="store_true", help="replicated runs: skip the naive / root-broadcast lines")
     ap.add_argument("--no-profile", action="store_true", help="no per-launch CUDA events in the timed region")
+    ap.add_argument("--capture", action="store_true",
+                    help="captured load (sllm_load_capture): the load recorded once as CUDA graphs outside the "
+                         "timed region (a1-a3 once), each step one replay (a4-a8) + wait -- repeated loads of one "
+                         "checkpoint, e.g. adapter swaps; no fan-out")
     ap.add_argument("--plumbing", action="store_true",
                     help="CPU-only dry run of the launch / rank / max-over-ranks plumbing (gloo, host memcpy in place "
                          "of the load; not a measurement)")
@@ -884,7 +888,16 @@ def main(argv=None):
     elif args.fanout in ("bcast", "allgather"):  # NCCL communicator over the process group
         comm = sllm.Comm.from_process_group(gpu) if world > 1 else sllm.Comm.init_rank(sllm.Comm.unique_id(), 1, 0, gpu)
 
+    captured = None
+    if args.capture:
+        if comm is not None:
+            fail_loudly("--capture has no fan-out")
+        captured = sllm.load_capture(sllm.Index.from_bytes(blob), bufs, gpus,
+                                     sllm.LoadConfig(**{**cfg.__dict__, "profile": 0}), bases, per_tensor)
+
     def step(prof: bool):
+        if captured is not None:  # one replay of the recorded graphs on the caller streams
+            return captured.replay(streams), captured.index
         # profile 3: per-launch CUDA events + in-kernel spans (two %globaltimer atomics per CTA)
         c = sllm.LoadConfig(**{**cfg.__dict__, "profile": 3 if prof else 0})
         ix = sllm.Index.from_bytes(blob)                  # a1: open + validate the index
@@ -927,6 +940,9 @@ def main(argv=None):
     # the last timed load's tensors vs the seeded payloads, byte for byte (untimed)
     bitexact = bitexact_sample(prev[0], inv, seed, torch) if prev is not None else None
     prev = None
+    if captured is not None:  # (its graphs and reserved destinations go before the e2e leg)
+        captured.free()
+        captured = None
     gc.unfreeze()
     if world > 1:
         dist.barrier()
@@ -1067,7 +1083,10 @@ def main(argv=None):
                     **({"same_gpu_plumbing_check": "all ranks on cuda:0 (gloo); not a scaling number"}
                        if SAME_GPU and world > 1 else {}),
                     **({"peer_wait": "host (load workers poll the peers' flags; no kernel waits on another rank)"}
-                       if os.environ.get("SLLM_PEER_WAIT") == "host" and args.fanout == "p2p" else {})}),
+                       if os.environ.get("SLLM_PEER_WAIT") == "host" and args.fanout == "p2p" else {}),
+                    **({"capture": "load recorded once as CUDA graphs outside the timed region (index parse and plan "
+                                   "once); step = one replay (transfer, verify, materialise) + wait"}
+                       if args.capture else {})}),
                 "time_to_loaded_model_s": ms_step * 1e-3, "step_ms": step_stats(ms_steps), "bitexact": bitexact,
                 "t_alloc_s": t_alloc, "t_setup_s": t_setup,
                 "b_h2d_measured_GBps": b_h2d, "frac_h2d": pcie_rate / b_h2d,

@@ -437,6 +437,28 @@ SLLM_API sllm_status sllm_load_files_start(const sllm_index* index, const sllm_l
                                            const int32_t* gpu, void* const* dst_base, void* const* dst_tensor,
                                            void* const* stream, int32_t io_threads, sllm_comm* comm, sllm_load** out);
 
+/* Captured load (latency-bound small checkpoints; CUDA graphs instead of
+ * a per-load host issue sequence).  sllm_load_capture plans the load exactly as
+ * sllm_load_start (same arguments, pinned sources, no fan-out, no files, no profiling) and
+ * records each partition's whole device work -- table upload, accumulator reset, the copy
+ * windows, the verify / scatter launches, the result read-back -- as one CUDA graph per
+ * partition, without moving any byte.  sllm_load_replay then loads the checkpoint again by
+ * launching those graphs (one cudaGraphLaunch per partition, no index walk, no worker
+ * hand-off, no per-window API calls) for repeated loads of the same checkpoint into the same
+ * destinations, e.g. swapping adapters in a serving loop (P:1253 LoRA loading).
+ *   sllm_load_replay: stream[p] = the caller's cudaStream_t (as void*) for partition p, the
+ *     replay queued on it (ordered after its earlier work; later work on it sees the bytes),
+ *     or NULL array / entry = a library stream.  SLLM_E_BUSY if the previous replay has not
+ *     been waited for.  The sources must hold the checkpoint's bytes when the replay runs.
+ *   sllm_load_wait reports the last replay (verification result, device time); tensor
+ *   handles and block checksums refer to the last waited replay.
+ * The destinations stay reserved (SLLM_E_BUSY for other loads) until sllm_load_free, which
+ * waits for the last replay and frees the graphs. */
+SLLM_API sllm_status sllm_load_capture(const sllm_index* index, const sllm_load_config* cfg,
+                                       const void* const* host_src, const int32_t* gpu,
+                                       void* const* dst_base, void* const* dst_tensor, sllm_load** out);
+SLLM_API sllm_status sllm_load_replay(sllm_load* load, void* const* stream);
+
 /* Block until every chunk (and fan-out round) has landed and been verified.  Returns
  * SLLM_E_CHECKSUM with rep->bad_partition / rep->bad_block naming the first failing
  * block, or the first CUDA/NCCL error.  Idempotent (returns the same status again).

@@ -131,6 +131,8 @@ SIGNATURES = {
     "sllm_load_start": (S, [P, C.POINTER(LoadConfig), PP, C.POINTER(C.c_int32), PP, PP, PP, P, PP]),
     "sllm_load_files_start": (S, [P, C.POINTER(LoadConfig), C.c_char_p, C.POINTER(C.c_int32), PP, PP, PP, C.c_int32,
                                   P, PP]),
+    "sllm_load_capture": (S, [P, C.POINTER(LoadConfig), PP, C.POINTER(C.c_int32), PP, PP, PP]),
+    "sllm_load_replay": (S, [P, PP]),
     "sllm_load_wait": (S, [P, C.POINTER(LoadReport)]),
     "sllm_load_tensor": (S, [P, C.c_char_p, C.POINTER(TensorHandle)]),
     "sllm_load_block_checksums": (S, [P, C.c_size_t, C.POINTER(C.POINTER(U64))]),

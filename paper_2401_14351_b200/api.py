@@ -659,6 +659,47 @@ def load_start(index: Index, sources: Dict[int, object], gpus: Dict[int, int], c
     return LoadResult(out, index, tensors, [dst_base, dst_tensor, st, bases, per_tensor, sources])
 
 
+class CapturedLoad(LoadResult):
+    """sllm_load_capture: the load recorded once as one CUDA graph per partition; every
+    ``replay()`` loads the checkpoint again into the same destinations (one graph launch per
+    partition) and ``wait()`` reports that replay's verification."""
+
+    def replay(self, streams: Optional[Dict[int, object]] = None) -> "CapturedLoad":
+        n = len(self.index.partitions)
+        st = None
+        if streams:
+            st = _ptr_array([streams[p].cuda_stream if p in streams else None for p in range(n)])
+        check(lib().sllm_load_replay(self._h, st))
+        return self
+
+
+def load_capture(index: Index, sources: Dict[int, object], gpus: Dict[int, int], config: Optional[LoadConfig] = None,
+                 bases: Optional[Dict[int, object]] = None, per_tensor: Optional[Dict[str, object]] = None
+                 ) -> CapturedLoad:
+    """sllm_load_capture over preallocated destinations (arguments as ``load_start``; no
+    fan-out, no streams: each ``replay`` takes them)."""
+    cfg = config or LoadConfig()
+    parts = index.partitions
+    n = len(parts)
+    src = [None] * n
+    gpu = (C.c_int32 * max(n, 1))()
+    for p, s in sources.items():
+        src[p] = s.ptr if isinstance(s, HostBuffer) else int(s)
+        gpu[p] = int(gpus[p])
+    dst_base = dst_tensor = None
+    if not cfg.scatter:
+        dst_base = _ptr_array([bases[p].data_ptr() if p in (bases or {}) else None for p in range(n)])
+    else:
+        dst_tensor = _ptr_array([per_tensor[t.name].data_ptr() if t.partition in sources else None
+                                 for t in index.tensors])
+    out = C.c_void_p()
+    ccfg = cfg.to_c()
+    check(lib().sllm_load_capture(index.handle, C.byref(ccfg), _ptr_array(src), gpu, dst_base, dst_tensor,
+                                  C.byref(out)))
+    tensors = _views(index, sources.keys(), bases, per_tensor, cfg.scatter)
+    return CapturedLoad(out, index, tensors, [dst_base, dst_tensor, bases, per_tensor, sources])
+
+
 def load_files(index: Index, directory: str, gpus: Dict[int, int], config: Optional[LoadConfig] = None,
                io_threads: int = 0, wait: bool = True, stream_of_caller: bool = True,
                bases: Optional[Dict[int, object]] = None, per_tensor: Optional[Dict[str, object]] = None,

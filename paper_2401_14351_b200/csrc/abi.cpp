@@ -23,7 +23,8 @@ uint64_t materialise_device(const sllm_index* idx, size_t p, const void* src, vo
 }  // namespace sllm
 
 sllm_load* sllm_load_create_internal(const sllm_index*, const sllm_load_config*, const void* const*, const int32_t*,
-                                     void* const*, void* const*, void* const*, sllm_comm*, const char*, int32_t);
+                                     void* const*, void* const*, void* const*, sllm_comm*, const char*, int32_t, bool capture = false);
+void sllm_load_replay_internal(sllm_load*, void* const*);
 sllm_status sllm_load_wait_internal(sllm_load*, sllm_load_report*);
 void sllm_load_tensor_internal(const sllm_load*, const char*, sllm_tensor_handle*);
 void sllm_load_block_checksums_internal(sllm_load*, size_t, const uint64_t**);
@@ -434,6 +435,21 @@ sllm_status sllm_load_files_start(const sllm_index* idx, const sllm_load_config*
   return guard_dev([&] {
     if (!out || !dir) fail(SLLM_E_INVALID, "null argument");
     *out = sllm_load_create_internal(idx, cfg, nullptr, gpu, dst_base, dst_tensor, stream, comm, dir, io_threads);
+  });
+}
+
+sllm_status sllm_load_capture(const sllm_index* idx, const sllm_load_config* cfg, const void* const* host_src,
+                              const int32_t* gpu, void* const* dst_base, void* const* dst_tensor, sllm_load** out) {
+  return guard_dev([&] {
+    if (!out) fail(SLLM_E_INVALID, "null out");
+    *out = sllm_load_create_internal(idx, cfg, host_src, gpu, dst_base, dst_tensor, nullptr, nullptr, nullptr, 0, true);
+  });
+}
+
+sllm_status sllm_load_replay(sllm_load* load, void* const* stream) {
+  return guard_dev([&] {
+    if (!load) fail(SLLM_E_INVALID, "null load");
+    sllm_load_replay_internal(load, stream);
   });
 }
 

@@ -156,6 +156,12 @@ struct PartJob {
   std::vector<uint64_t> kev_bytes;  // bytes covered by each timed kernel launch
   uint64_t kernel_bytes = 0;
   double kernel_ms = 0, copy_ms = 0, kernel_span_ms = 0;
+  // captured loads (sllm_load_capture): the job's work as one CUDA graph, replayed by
+  // sllm_load_replay; its tables / result word live in a pinned block of its own
+  bool capture = false;
+  cudaGraphExec_t exec = nullptr;
+  uint8_t* gstage = nullptr;
+  cudaStream_t rstream = nullptr;  // replay stream when the caller passes none
   bool finished = false;           // run_job_guarded returned (guarded by sllm_load::issue_mu)
   std::vector<cudaStream_t> used;  // streams this job queued work on (drained on failure)
   StreamSet* ss = nullptr;         // leased from the GPU's DeviceCtx for the job's lifetime
@@ -176,6 +182,12 @@ struct sllm_load {
   sllm_load_report rep{};
   std::mutex issue_mu;                 // jobs report "all my work is enqueued" (or failed)
   std::condition_variable issue_cv;
+  // captured load: replays issued / the last one reported by wait
+  bool graph = false;
+  uint64_t replays = 0;
+  bool replay_pending = false;
+  std::chrono::steady_clock::time_point t_replay;
+  uint64_t t_replay_issue_ns = 0;
 };
 
 namespace sllm {
@@ -590,7 +602,13 @@ static void run_job(sllm_load* L, PartJob& j) {
     SLLM_CUDA(cudaMallocAsync(&st, (size_t)P.nslot * P.slot_bytes, s0));
     j.staging = static_cast<uint8_t*>(st);
   }
-  uint8_t* h = j.ss->host_stage(up_bytes + 256 + kt_bytes);
+  uint8_t* h = nullptr;
+  if (j.capture) {  // the graph's upload node reads this block at every replay: the job owns it
+    SLLM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&j.gstage), up_bytes + 256, cudaHostAllocDefault));
+    h = j.gstage;
+  } else {
+    h = j.ss->host_stage(up_bytes + 256 + kt_bytes);
+  }
   j.h_result = h + up_bytes;  // 16 bytes: first failing block, peer-wait result
   std::memcpy(h, j.segs.data(), j.segs.size() * sizeof(Seg));
   if (!j.gran_seg.empty()) std::memcpy(h + seg_bytes, j.gran_seg.data(), j.gran_seg.size() * 4);
@@ -610,6 +628,12 @@ static void run_job(sllm_load* L, PartJob& j) {
   j.d_tickets = tk_bytes ? reinterpret_cast<unsigned long long*>(base + up_bytes + acc_bytes + tab_bytes + kt_bytes)
                          : nullptr;
   j.ticket_base.clear();
+  if (j.capture) {
+    // everything from the table upload to the result word becomes the job's graph (the
+    // scratch / staging allocations above are done first: a replay reuses them)
+    SLLM_CUDA(cudaStreamSynchronize(s0));
+    SLLM_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed));
+  }
   SLLM_CUDA(cudaMemcpyAsync(base, h, up_bytes, cudaMemcpyHostToDevice, s0));
   SLLM_CUDA(cudaMemsetAsync(base + up_bytes, 0, zero_bytes, s0));
   SLLM_CUDA(cudaEventRecord(j.ev[0], s0));
@@ -804,6 +828,19 @@ static void run_job(sllm_load* L, PartJob& j) {
   if (j.d_ktime && !j.kev.empty())  // profile 3: the timed launches' in-kernel stamps
     SLLM_CUDA(cudaMemcpyAsync(j.h_ktime, j.d_ktime, 4 * sizeof(unsigned long long) * std::min(j.kev.size(), kMaxKtime),
                               cudaMemcpyDeviceToHost, s0));
+  if (j.capture) {  // the job's graph: instantiated here, run by sllm_load_replay
+    cudaGraph_t g = nullptr;
+    SLLM_CUDA(cudaStreamEndCapture(s0, &g));
+    const cudaError_t e = cudaGraphInstantiate(&j.exec, g, 0);
+    cudaGraphDestroy(g);
+    SLLM_CUDA(e);
+    cudaEventDestroy(P.copied);
+    for (auto& ev : P.freed) cudaEventDestroy(ev);
+    j.t_issue_ns = now_ns() - t0;
+    std::lock_guard<std::mutex> lk(L->issue_mu);
+    j.issue_ok = j.issue_signalled = true;
+    return;
+  }
   {  // every command of this job is enqueued: the caller's stream may now wait on ev[1]
     std::lock_guard<std::mutex> g(L->issue_mu);
     j.issue_ok = j.issue_signalled = true;
@@ -937,6 +974,16 @@ static void run_job_guarded(sllm_load* L, PartJob& j) {
     // a failure part-way through issuing: let what was queued finish before the scratch,
     // staging and events it uses can be released by sllm_load_free
     cudaSetDevice(j.gpu);
+    if (j.capture)  // (a failure inside a capture: end it so the streams can be reused)
+      for (cudaStream_t st : j.used) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+          cudaGraph_t g = nullptr;
+          cudaStreamEndCapture(st, &g);
+          if (g) cudaGraphDestroy(g);
+        }
+        cudaGetLastError();
+      }
     for (cudaStream_t st : j.used) cudaStreamSynchronize(st);
     cudaGetLastError();
   }
@@ -958,10 +1005,13 @@ static void run_job_guarded(sllm_load* L, PartJob& j) {
 
 using namespace sllm;
 
+void sllm_load_free_internal(sllm_load* L);
+
 sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_config* cfg_in, const void* const* host_src,
                                      const int32_t* gpu, void* const* dst_base, void* const* dst_tensor,
-                                     void* const* stream, sllm_comm* comm, const char* dir, int32_t io_threads) {
-  NvtxRange nv("sllm.load_start");
+                                     void* const* stream, sllm_comm* comm, const char* dir, int32_t io_threads,
+                                     bool capture) {
+  NvtxRange nv(capture ? "sllm.load_capture" : "sllm.load_start");
   if (!idx) fail(SLLM_E_INVALID, "null index");
   if (!idx->sealed) fail(SLLM_E_INVALID, "index is planned but not sealed");
   sllm_load_config cfg{};
@@ -1010,6 +1060,12 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   } else if (cfg.fanout != SLLM_FANOUT_NONE) {
     fail(SLLM_E_INVALID, "unknown fan-out");
   }
+  if (capture) {  // a captured load replays one fixed sequence of device work
+    if (dir || cfg.mode == SLLM_MODE_GDS) fail(SLLM_E_INVALID, "sllm_load_capture loads from pinned sources only");
+    if (cfg.fanout != SLLM_FANOUT_NONE) fail(SLLM_E_INVALID, "sllm_load_capture has no fan-out");
+    cfg.profile = 0;
+    stream = nullptr;  // (the replay takes the streams)
+  }
   if ((!host_src && !dir) || !gpu) fail(SLLM_E_INVALID, "null host_src / gpu array");
   if (scatter && !dst_tensor) fail(SLLM_E_INVALID, "scatter modes need dst_tensor");
   if (!scatter && !dst_base) fail(SLLM_E_INVALID, "contiguous modes need dst_base");
@@ -1017,6 +1073,7 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   std::unique_ptr<sllm_load> L(new sllm_load);
   L->idx = idx;
   L->cfg = cfg;
+  L->graph = capture;
   L->comm = comm;
   L->t0 = std::chrono::steady_clock::now();
   if (scatter) L->dst_tensor.assign(dst_tensor, dst_tensor + idx->tensors.size());
@@ -1089,6 +1146,7 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
         fail(SLLM_E_INVALID, "zero-copy modes need a 16-byte aligned host source");
     }
     build_segments(*idx, j, scatter, L->dst_tensor, cfg.chunk_bytes);
+    j.capture = capture;
     L->jobs.push_back(std::move(j));
   }
   // busy set
@@ -1148,6 +1206,24 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
       j.issue_signalled = j.finished = true;
     }
   }
+  if (capture) {  // every job's graph is built before sllm_load_capture returns
+    {
+      std::unique_lock<std::mutex> lk(L->issue_mu);
+      L->issue_cv.wait(lk, [&] {
+        for (auto& j : L->jobs)
+          if (!j.finished) return false;
+        return true;
+      });
+    }
+    for (auto& j : L->jobs)
+      if (j.status != SLLM_OK) {
+        const sllm_status st = j.status;
+        const std::string err = j.error;
+        sllm_load_free_internal(L.release());
+        fail(st, err);
+      }
+    return L.release();
+  }
   // Caller-stream ordering without a device-side gate: a stream waiting for work that is not
   // yet enqueued can block, through the few hardware queues the context's streams share,
   // work this or another load enqueues later (a deadlock seen with concurrent gated loads).
@@ -1169,7 +1245,55 @@ sllm_load* sllm_load_create_internal(const sllm_index* idx, const sllm_load_conf
   return L.release();
 }
 
+// Captured load: the last replay's completion and verification result (idempotent until the
+// next replay).
+static void join_replay(sllm_load* L) {
+  if (!L->replay_pending) return;
+  L->replay_pending = false;
+  sllm_load_report& r = L->rep;
+  r = sllm_load_report{};
+  r.bad_partition = -1;
+  r.bad_block = ~0ull;
+  r.mode = L->cfg.mode;
+  sllm_status st = SLLM_OK;
+  for (auto& j : L->jobs) {
+    cudaSetDevice(j.gpu);
+    cudaError_t e = cudaEventSynchronize(j.ev[1]);
+    float ms = 0;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, j.ev[0], j.ev[1]);
+    if (e != cudaSuccess && st == SLLM_OK) {
+      cudaGetLastError();
+      st = SLLM_E_CUDA;
+      set_last_error(std::string("replay: ") + cudaGetErrorString(e));
+    }
+    uint64_t tail[2] = {};
+    std::memcpy(tail, j.h_result, 16);  // written by the graph's last node
+    j.h_bad = tail[0];
+    j.h_cs_valid = false;
+    for (uint32_t ti : L->idx->parts[j.p].by_offset) r.payload_bytes += L->idx->tensors[ti].nbytes;
+    r.transferred_bytes += j.transferred;
+    r.chunks += j.chunks;
+    r.kernel_launches += j.launches;
+    r.copy_calls += j.copies;
+    r.t_device_ms_max = std::max(r.t_device_ms_max, (double)ms);
+    if (st == SLLM_OK && j.h_bad != ~0ull && r.bad_partition < 0) {
+      r.bad_partition = (int32_t)j.p;
+      r.bad_block = j.h_bad;
+    }
+  }
+  r.t_issue_ns_max = L->t_replay_issue_ns;
+  if (st == SLLM_OK && r.bad_partition >= 0) {
+    st = SLLM_E_CHECKSUM;
+    set_last_error("checksum mismatch in partition " + std::to_string(r.bad_partition) + ", block " +
+                   std::to_string(r.bad_block));
+  }
+  r.t_total_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() -
+                                                                                L->t_replay).count();
+  L->result = st;
+}
+
 static void join_load(sllm_load* L) {
+  if (L->graph) return join_replay(L);
   if (L->joined) return;
   {
     std::unique_lock<std::mutex> lk(L->issue_mu);
@@ -1283,15 +1407,46 @@ void sllm_load_block_checksums_internal(sllm_load* L, size_t p, const uint64_t**
 
 void sllm_load_free_internal(sllm_load* L) {
   join_load(L);
+  if (L->graph) {  // the destinations were reserved for the captured load's lifetime
+    std::lock_guard<std::mutex> g(g_busy_mu);
+    for (const void* k : L->busy_keys) g_busy.erase(k);
+    L->busy_keys.clear();
+  }
   for (auto& j : L->jobs) {
     if (j.gpu >= 0) cudaSetDevice(j.gpu);
     DeviceCtx& dc = device_ctx(j.gpu);
+    if (j.exec) cudaGraphExecDestroy(j.exec);
+    if (j.rstream) cudaStreamDestroy(j.rstream);
     if (j.scratch) cudaFreeAsync(j.scratch, dc.misc);
     if (j.staging) cudaFreeAsync(j.staging, dc.misc);
+    if (j.gstage) cudaFreeHost(j.gstage);  // (join_load above waited for the last replay)
     for (auto& e : j.ev)
       if (e) cudaEventDestroy(e);
   }
   delete L;
+}
+
+// One replay of a captured load: per job, one graph launch on its stream between two timing
+// events (the second also marks completion for sllm_load_wait).
+void sllm_load_replay_internal(sllm_load* L, void* const* stream) {
+  if (!L->graph) fail(SLLM_E_INVALID, "not a captured load (sllm_load_capture)");
+  if (L->replay_pending) fail(SLLM_E_BUSY, "the previous replay has not been waited for");
+  const uint64_t t0 = now_ns();
+  L->t_replay = std::chrono::steady_clock::now();
+  for (auto& j : L->jobs) {
+    SLLM_CUDA(cudaSetDevice(j.gpu));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream[j.p]) : nullptr;
+    if (!st) {
+      if (!j.rstream) SLLM_CUDA(cudaStreamCreateWithFlags(&j.rstream, cudaStreamNonBlocking));
+      st = j.rstream;
+    }
+    SLLM_CUDA(cudaEventRecord(j.ev[0], st));
+    SLLM_CUDA(cudaGraphLaunch(j.exec, st));
+    SLLM_CUDA(cudaEventRecord(j.ev[1], st));
+  }
+  L->replays++;
+  L->replay_pending = true;
+  L->t_replay_issue_ns = now_ns() - t0;
 }
 
 void sllm_device_trim_internal(int32_t gpu, uint64_t keep_bytes) {
