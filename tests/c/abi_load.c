@@ -126,6 +126,32 @@ int main(void) {
     if (rep.payload_bytes == 0 || rep.bad_partition != -1) { fprintf(stderr, "report\n"); return 1; }
     sllm_load_free(ld);
   }
+  /* captured load: no byte moves at capture; two replays load every partition again */
+  {
+    sllm_load_config cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.chunk_bytes = 128 << 10;
+    cfg.verify = 1;
+    for (size_t p = 0; p < nparts; ++p) CUDA(cudaMemset(dbase[p], 0xEE, len[p]));
+    sllm_load* cap = NULL;
+    CHECK(sllm_load_capture(idx, &cfg, (const void* const*)host, gpu, dbase, NULL, &cap));
+    for (int r = 0; r < 3; ++r) {
+      for (size_t p = 0; p < nparts; ++p) {
+        uint8_t* back = (uint8_t*)malloc(len[p]);
+        CUDA(cudaMemcpy(back, dbase[p], len[p], cudaMemcpyDeviceToHost));
+        const int loaded = memcmp(back, host[p], len[p]) == 0;
+        free(back);
+        if (loaded != (r > 0)) { fprintf(stderr, "capture: replay %d partition %zu\n", r, p); return 1; }
+      }
+      if (r == 2) break;
+      for (size_t p = 0; p < nparts && r == 1; ++p) CUDA(cudaMemset(dbase[p], 0x11, len[p]));
+      CHECK(sllm_load_replay(cap, NULL));
+      sllm_load_report rep;
+      CHECK(sllm_load_wait(cap, &rep));
+      if (rep.payload_bytes == 0 || rep.bad_partition != -1) { fprintf(stderr, "capture report\n"); return 1; }
+    }
+    sllm_load_free(cap);
+  }
   /* a corrupted source byte is reported as (partition, block) */
   ((uint8_t*)host[1])[70000] ^= 1;
   {
