@@ -3,6 +3,7 @@ free each time, rotating modes), watching device free memory and host RSS for le
 
     python tools/soak.py [--config opt-6.7b] [--loads 100]
     python tools/soak.py --config lora-70b-r32 --loads 300 --p2p 2   # in-process P2P group
+    python tools/soak.py --config lora-70b-r32 --loads 500 --capture # captured load, replays
 
 Prints one JSON line: loads, failures, seconds, device free memory and RSS before / after
 (after the library's idle cache is trimmed), and the GB/s range."""
@@ -28,6 +29,8 @@ def main():
     ap.add_argument("--loads", type=int, default=100)
     ap.add_argument("--p2p", type=int, default=0, help="R > 1: an in-process P2P group of R replicas on GPU 0 "
                     "(event-ordered), every load verified on every replica")
+    ap.add_argument("--capture", action="store_true", help="one captured load, --loads replays (rotating modes "
+                    "= one capture per mode)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -40,6 +43,8 @@ def main():
     table = idx.block_checksums(0)
     if args.p2p > 1:
         return soak_p2p(args, sllm, torch, np, idx, bufs, table)
+    if args.capture:
+        return soak_capture(args, sllm, torch, np, idx, bufs, table)
     modes = ["ce", "zerocopy", "scatter_ce", "scatter_zc", "auto"]
     # warm once per mode (pools, module load), then measure the baseline
     for m in modes:
@@ -72,6 +77,38 @@ def main():
                       "maxrss_GB": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6,
                       "per_mode_GBps": {m: {"min": min(v), "median": float(np.median(v)), "slowest_load": int(np.argmin(v))}
                                         for m, v in by_mode.items() if v}}), flush=True)
+
+
+def soak_capture(args, sllm, torch, np, idx, bufs, table):
+    """Captured loads: one capture per mode, then --loads replays rotating over them; every
+    replay's block checksums must equal the index table; device / host memory watched."""
+    modes = ["ce", "zerocopy", "scatter_ce", "scatter_zc"]
+    caps = []
+    for m in modes:
+        cfg = sllm.LoadConfig(chunk_bytes=64 << 20, mode=m)
+        bases, per = sllm.allocate(idx, {0: 0}, cfg.scatter)
+        caps.append(sllm.load_capture(idx, bufs, {0: 0}, cfg, bases, per))
+        caps[-1].replay().wait()  # warm
+    torch.cuda.synchronize()
+    free0, rss0 = torch.cuda.mem_get_info(0)[0], rss_gb()
+    rates, failures = [], 0
+    t0 = time.perf_counter()
+    for i in range(args.loads):
+        c = caps[i % len(caps)]
+        ts = time.perf_counter()
+        c.replay().wait()
+        rates.append(idx.partitions[0].length / (time.perf_counter() - ts) / 1e9)
+        failures += not np.array_equal(c.block_checksums(0), table)
+    dt = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    free1, rss1 = torch.cuda.mem_get_info(0)[0], rss_gb()
+    for c in caps:
+        c.free()
+    print(json.dumps({"config": args.config, "captured_modes": modes, "replays": args.loads, "failures": failures,
+                      "seconds": dt, "GBps_min": min(rates), "GBps_median": float(np.median(rates)),
+                      "device_free_GB_before": free0 / 1e9, "device_free_GB_after": free1 / 1e9,
+                      "device_leak_GB": (free0 - free1) / 1e9, "rss_GB_before": rss0, "rss_GB_after": rss1}),
+          flush=True)
 
 
 def soak_p2p(args, sllm, torch, np, idx, bufs, table):
