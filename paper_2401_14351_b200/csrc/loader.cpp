@@ -1433,6 +1433,7 @@ void sllm_load_replay_internal(sllm_load* L, void* const* stream) {
   if (L->replay_pending) fail(SLLM_E_BUSY, "the previous replay has not been waited for");
   const uint64_t t0 = now_ns();
   L->t_replay = std::chrono::steady_clock::now();
+  L->replay_pending = true;  // (set first: a failure part-way still gets the launched graphs waited for)
   for (auto& j : L->jobs) {
     SLLM_CUDA(cudaSetDevice(j.gpu));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream[j.p]) : nullptr;
@@ -1445,7 +1446,6 @@ void sllm_load_replay_internal(sllm_load* L, void* const* stream) {
     SLLM_CUDA(cudaEventRecord(j.ev[1], st));
   }
   L->replays++;
-  L->replay_pending = true;
   L->t_replay_issue_ns = now_ns() - t0;
 }
 
