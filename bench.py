@@ -84,7 +84,7 @@ def parse(argv=None):
     ap.add_argument("--capture", action="store_true",
                     help="captured load (sllm_load_capture): the load recorded once as CUDA graphs outside the "
                          "timed region (a1-a3 once), each step one replay (a4-a8) + wait -- repeated loads of one "
-                         "checkpoint, e.g. adapter swaps; no fan-out")
+                         "checkpoint from the same pinned source into the same destinations; no fan-out")
     ap.add_argument("--plumbing", action="store_true",
                     help="CPU-only dry run of the launch / rank / max-over-ranks plumbing (gloo, host memcpy in place "
                          "of the load; not a measurement)")

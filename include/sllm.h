@@ -445,7 +445,10 @@ SLLM_API sllm_status sllm_load_files_start(const sllm_index* index, const sllm_l
  * partition, without moving any byte.  sllm_load_replay then loads the checkpoint again by
  * launching those graphs (one cudaGraphLaunch per partition, no index walk, no worker
  * hand-off, no per-window API calls) for repeated loads of the same checkpoint into the same
- * destinations, e.g. swapping adapters in a serving loop (P:1253 LoRA loading).
+ * destinations from the same pinned source (the graphs hold the source, destination and
+ * table addresses and the checkpoint's expected checksums): e.g. an adapter kept resident in
+ * the pinned pool and re-loaded into its GPU slot whenever it is needed again (P:1253 LoRA
+ * loading); another checkpoint -- another adapter -- is another captured load.
  *   sllm_load_replay: stream[p] = the caller's cudaStream_t (as void*) for partition p, the
  *     replay queued on it (ordered after its earlier work; later work on it sees the bytes),
  *     or NULL array / entry = a library stream.  SLLM_E_BUSY if the previous replay has not
